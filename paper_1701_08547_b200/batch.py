@@ -1,0 +1,675 @@
+"""Batch entry points of the B200 backend (the additions of SURVEY §8(b)).
+
+* ``occupancy_batch``  -- Kd: OccupancyResult fields for N launches.
+* ``suggest_batch``    -- K4: suggest() for many (arch, kernel) pairs.
+* ``aggregate_batch``  -- K0: aggregate() for many instruction streams.
+* ``feature_score``    -- K1: intensity / Eq. 6 cost / utilisation.
+* ``ScorePlan`` / ``score_space`` -- K2+K3: score an Orio-style space and
+  return the top-k configurations per (kernel, arch) segment.
+
+All device memory is torch-allocated (plumbing only); every number comes
+from liboccx.so.  Host code packs inputs, launches, and unpacks results.
+"""
+
+from __future__ import annotations
+
+import bisect
+import sys
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+from .arch import ArchSpec, COST_KEY_OF_MAJOR, pack_archs
+from .errors import DeviceError, IllegalLaunchError
+from .mix import (CATEGORY_OF, COUNTABLE, CPI_ROW, DEFAULT_OPCLASSES, DEFAULT_THROUGHPUT,
+                  DEVICE_ID, Category, InstructionMix, OpClass, ThroughputTable,
+                  classify_signature)
+from .occupancy import (LIMITER_OF_CODE, MODE_CODE, LaunchInput, Mode, OccupancyResult,
+                        SuggestionReport, thread_candidates)
+from .resources import register_operand_count
+from .tuning import TuningSpace, grid_size, membership_masks
+
+# CPython's float sum() changed in 3.12 (compensated); K1 follows the
+# interpreter running this process.
+SUM_MODE = 0 if sys.version_info >= (3, 12) else 1
+U32_MAX = 0xFFFFFFFF
+IDX_MASK = (1 << 34) - 1
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: the occx backend runs on the GPU only")
+    return torch
+
+
+def _to_device(arr: np.ndarray):
+    torch = _torch()
+    flat = np.ascontiguousarray(arr).view(np.uint8).reshape(-1)
+    t = torch.empty(max(flat.size, 1), dtype=torch.uint8, device="cuda")
+    if flat.size:
+        t[: flat.size].copy_(torch.from_numpy(flat))
+    return t
+
+
+def _empty(nbytes: int):
+    torch = _torch()
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device="cuda")
+
+
+def _to_host(t, dtype: np.dtype, count: int) -> np.ndarray:
+    if count == 0:
+        return np.zeros(0, dtype)
+    raw = t[: count * dtype.itemsize].cpu().numpy()
+    return raw.view(dtype).copy()
+
+
+def _arch_list(archs) -> list[ArchSpec]:
+    return [archs] if isinstance(archs, ArchSpec) else list(archs)
+
+
+# ---------------------------------------------------------------------------
+# Kd: occupancy dump
+# ---------------------------------------------------------------------------
+
+@dataclass
+class OccBatch:
+    """Columnar OccupancyResult batch (occupancy.py:55-65)."""
+
+    raw: np.ndarray
+    mode: Mode
+
+    def __len__(self):
+        return len(self.raw)
+
+    def __getattr__(self, name):
+        raw = self.__dict__.get("raw")
+        if raw is not None and name in raw.dtype.names:
+            return raw[name]
+        raise AttributeError(name)
+
+    @property
+    def wpb(self):
+        return self.raw["wpb"]
+
+    def result(self, i: int) -> OccupancyResult:
+        r = self.raw[i]
+        if r["status"] == 2:
+            raise IllegalLaunchError("threads_per_block outside the architecture's range")
+        if r["status"]:
+            raise ValueError("invalid candidate record")
+        return OccupancyResult(
+            warps_per_block=int(r["wpb"]), limit_warps=int(r["limit_warps"]),
+            limit_regs=int(r["limit_regs"]), limit_smem=int(r["limit_smem"]),
+            active_blocks=int(r["active_blocks"]), active_warps=int(r["active_warps"]),
+            occupancy=float(r["occupancy"]), limiter=LIMITER_OF_CODE[int(r["limiter"])],
+            mode=self.mode)
+
+
+def pack_launches(launches, arch_index=None) -> np.ndarray:
+    """(T, R, S) triples -> occx_cand_t records.  Values are clamped to the
+    record's field widths in a way that keeps every result unchanged: any
+    T > 65535, R > 65535 or S > 2^32-1 is already beyond every device-
+    representable architecture's limit (arch.device_limits_ok)."""
+    a = np.asarray(launches, dtype=np.int64).reshape(-1, 3)
+    rec = np.zeros(len(a), _lib.CAND)
+    if (a < 0).any():
+        raise IllegalLaunchError("resource amounts must be non-negative")
+    rec["threads"] = np.minimum(a[:, 0], 0xFFFF)
+    rec["regs"] = np.minimum(a[:, 1], 0xFFFF)
+    rec["smem"] = np.minimum(a[:, 2], U32_MAX)
+    if arch_index is not None:
+        rec["arch"] = np.asarray(arch_index, dtype=np.uint8)
+    return rec
+
+
+def occupancy_records(archs, d_records, n: int, mode: Mode = Mode.CORRECTED, d_out=None):
+    """Device-level Kd: records already in HBM -> occx_occ_t array (device)."""
+    torch = _torch()
+    h_archs = pack_archs(_arch_list(archs))
+    out = d_out if d_out is not None else _empty(n * _lib.OCC.itemsize)
+    _lib.check(_lib.load().occx_occupancy_batch(
+        _lib.ctx(), _lib.ptr(h_archs), len(h_archs), _lib.ptr(d_records), n,
+        MODE_CODE[Mode(mode)], _lib.ptr(out), _lib.stream_ptr()), "occx_occupancy_batch")
+    del torch
+    return out
+
+
+def occupancy_batch(archs, launches, mode: Mode = Mode.CORRECTED, arch_index=None) -> OccBatch:
+    """occupancy() for many launches on the GPU (ref occupancy.py:163-195)."""
+    mode = Mode(mode)
+    rec = pack_launches(launches, arch_index)
+    d_rec = _to_device(rec)
+    out = occupancy_records(archs, d_rec, len(rec), mode)
+    return OccBatch(_to_host(out, _lib.OCC, len(rec)), mode)
+
+
+# ---------------------------------------------------------------------------
+# K4: suggest
+# ---------------------------------------------------------------------------
+
+def suggest_batch(requests, mode: Mode = Mode.CORRECTED) -> list[SuggestionReport]:
+    """suggest(arch, resources, mode, dynamic_shared_mem) for many requests
+    (ref occupancy.py:232-279).  requests: (arch, resources[, dynamic])."""
+    mode = Mode(mode)
+    archs: list[ArchSpec] = []
+    index: dict[int, int] = {}
+    inp = np.zeros(len(requests), _lib.SUGG_IN)
+    for i, req in enumerate(requests):
+        arch, res = req[0], req[1]
+        dyn = req[2] if len(req) > 2 else 0
+        if id(arch) not in index:
+            index[id(arch)] = len(archs)
+            archs.append(arch)
+        regs = res.registers_per_thread
+        smem = res.static_shared_mem + dyn
+        if regs < 0 or smem < 0:
+            raise ValueError("negative resource footprint")
+        inp[i] = (index[id(arch)], min(regs, U32_MAX), min(smem, U32_MAX), 0)
+    if not requests:
+        return []
+    h_archs = pack_archs(archs)
+    d_in = _to_device(inp)
+    d_out = _empty(len(inp) * _lib.SUGG.itemsize)
+    _lib.check(_lib.load().occx_suggest_batch(
+        _lib.ctx(), _lib.ptr(h_archs), len(h_archs), _lib.ptr(d_in), len(inp),
+        MODE_CODE[mode], _lib.ptr(d_out), _lib.stream_ptr()), "occx_suggest_batch")
+    out = _to_host(d_out, _lib.SUGG, len(inp))
+    reports = []
+    for i, req in enumerate(requests):
+        arch, res = req[0], req[1]
+        o = out[i]
+        st = int(o["status"])
+        if st == 2:
+            raise IllegalLaunchError(
+                f"{res.registers_per_thread} registers/thread or "
+                f"{int(inp[i]['smem'])} bytes of shared memory exceed {arch.name}")
+        if st == 10:
+            raise IndexError("tuple index out of range")
+        _lib.check(st, "occx_suggest_batch")
+        reports.append(SuggestionReport(
+            thread_candidates=thread_candidates(arch),
+            registers_used=res.registers_per_thread,
+            register_headroom=int(o["register_headroom"]),
+            smem_budget=int(o["smem_budget"]),
+            best_occupancy=float(o["best_occupancy"]),
+            best_threads=int(o["best_threads"]),
+            best_blocks=int(o["best_blocks"])))
+    return reports
+
+
+# ---------------------------------------------------------------------------
+# K0: aggregate
+# ---------------------------------------------------------------------------
+
+class SignatureTable:
+    """Interns (opcode, modifiers) signatures; the LUT holds classify()
+    of each signature (ref mix.py:176-187), evaluated once per distinct
+    signature rather than once per instruction."""
+
+    def __init__(self, table: dict[str, OpClass] = DEFAULT_OPCLASSES):
+        self.table = table
+        self.ids: dict[tuple, int] = {}
+        self.classes: list[int] = []
+
+    def intern(self, opcode: str, modifiers) -> int:
+        key = (opcode, tuple(modifiers))
+        sid = self.ids.get(key)
+        if sid is None:
+            sid = len(self.classes)
+            if sid >= 65536:
+                raise DeviceError("more than 65536 distinct instruction signatures")
+            self.ids[key] = sid
+            self.classes.append(DEVICE_ID[classify_signature(opcode, key[1], self.table)])
+        return sid
+
+    def lut(self) -> np.ndarray:
+        return np.asarray(self.classes or [DEVICE_ID[OpClass.UNCLASSIFIED]], np.uint8)
+
+
+def pack_instructions(kernels, sigs: SignatureTable):
+    """Instruction streams -> (u32 records, u64 CSR offsets)."""
+    recs: list[int] = []
+    offs = [0]
+    for instrs in kernels:
+        for ins in instrs:
+            sid = sigs.intern(ins.opcode, ins.modifiers)
+            nreg = register_operand_count(ins)
+            if nreg > 255:
+                raise DeviceError("instruction with more than 255 register operands")
+            recs.append(sid | (nreg << 16) | ((1 if ins.predicate else 0) << 24))
+        offs.append(len(recs))
+    return np.asarray(recs, np.uint32), np.asarray(offs, np.uint64)
+
+
+def mix_reduce(d_instr, d_off, n_kernels: int, d_lut, n_sig: int, d_out=None):
+    """Device-level K0: CSR records in HBM -> occx_mix_t array (device)."""
+    out = d_out if d_out is not None else _empty(n_kernels * _lib.MIX.itemsize)
+    _lib.check(_lib.load().occx_mix_reduce(
+        _lib.ctx(), _lib.ptr(d_instr), _lib.ptr(d_off), n_kernels, _lib.ptr(d_lut), n_sig,
+        _lib.ptr(out), _lib.stream_ptr()), "occx_mix_reduce")
+    return out
+
+
+def mix_from_record(m) -> InstructionMix:
+    """occx_mix_t -> InstructionMix with dict insertion order restored."""
+    present = [(int(m["first_key"][c]), c) for c in range(15) if m["counts"][c]]
+    present.sort()
+    counts = {COUNTABLE[c]: int(m["counts"][c]) for _, c in present}
+    return InstructionMix(counts, int(m["reg_operands"]))
+
+
+def aggregate_batch(kernels, table: dict[str, OpClass] = DEFAULT_OPCLASSES) -> list[InstructionMix]:
+    """aggregate() over many instruction streams on the GPU (K0)."""
+    kernels = [list(k) for k in kernels]
+    if not kernels:
+        return []
+    sigs = SignatureTable(table)
+    rec, off = pack_instructions(kernels, sigs)
+    lut = sigs.lut()
+    d_out = mix_reduce(_to_device(rec), _to_device(off), len(kernels), _to_device(lut), len(lut))
+    out = _to_host(d_out, _lib.MIX, len(kernels))
+    return [mix_from_record(m) for m in out]
+
+
+# ---------------------------------------------------------------------------
+# K1: feature scoring
+# ---------------------------------------------------------------------------
+
+_CATS = (Category.FLOPS, Category.MEM, Category.CTRL, Category.REG)
+_CPI_CLASS = {row: cls for cls, row in CPI_ROW.items()}
+
+
+def pack_mixes(mixes: Sequence[InstructionMix]) -> np.ndarray:
+    out = np.zeros(len(mixes), _lib.MIX)
+    out["first_key"] = U32_MAX
+    for i, m in enumerate(mixes):
+        for rank, (cls, n) in enumerate(m.counts.items()):
+            if n > U32_MAX:
+                raise DeviceError("per-class count above 2^32-1")
+            d = DEVICE_ID[cls]
+            out[i]["counts"][d] = n
+            out[i]["first_key"][d] = rank
+        out[i]["reg_operands"] = m.reg_operands
+        out[i]["n_instr"] = min(m.total_instructions, U32_MAX)
+    return out
+
+
+def cost_key_of_cc(cc: float) -> int:
+    return COST_KEY_OF_MAJOR.get(int(cc), -1)
+
+
+@dataclass
+class Features:
+    cost: float
+    coefficients: dict
+    cycles: dict
+    shares: dict
+    per_class: dict
+
+
+@dataclass
+class FeatureBatch:
+    sums: np.ndarray      # occx_mixsum_t[n_mix]
+    feat: np.ndarray      # occx_feat_t[n_mix * n_col]
+    n_col: int
+    mixes: list = field(default_factory=list)
+    ccs: list = field(default_factory=list)
+
+    @property
+    def intensity(self) -> list[float]:
+        return [float(x) for x in self.sums["intensity"]]
+
+    def one(self, m: int, j: int) -> Features:
+        f = self.feat[m * self.n_col + j]
+        st = int(f["status"])
+        cc = self.ccs[j]
+        if st == 3:
+            from .mix import sm_key
+            sm_key(cc)                      # raises UnsupportedArchitectureError
+        if st == 9:
+            raise KeyError("throughput table has no entry for a class in use")
+        _lib.check(st, "occx_feature_score")
+        mix = self.mixes[m]
+        per_class = {}
+        for cls in mix.counts:
+            if cls is not OpClass.UNCLASSIFIED and mix.counts[cls]:
+                per_class[cls] = float(f["per_class"][CPI_ROW[cls]])
+        if mix.reg_operands:
+            per_class[OpClass.REGS] = float(f["per_class"][CPI_ROW[OpClass.REGS]])
+        return Features(
+            cost=float(f["cost"]),
+            coefficients={c: float(f["coef"][i]) for i, c in enumerate(_CATS)},
+            cycles={c: float(f["cycles"][i]) for i, c in enumerate(_CATS)},
+            shares={c: float(f["shares"][i]) for i, c in enumerate(_CATS)},
+            per_class=per_class)
+
+
+def feature_records(d_mix, n_mix: int, cols: Sequence[int], cpi: np.ndarray, scale: float,
+                    sum_mode: int = SUM_MODE):
+    """Device-level K1 -> (d_sum, d_feat)."""
+    h_cols = np.asarray(list(cols) or [0], np.int32)
+    h_cpi = np.ascontiguousarray(cpi, np.float64).reshape(4, 16)
+    d_sum = _empty(n_mix * _lib.MIXSUM.itemsize)
+    d_feat = _empty(n_mix * max(len(cols), 1) * _lib.FEAT.itemsize)
+    _lib.check(_lib.load().occx_feature_score(
+        _lib.ctx(), _lib.ptr(d_mix), n_mix, _lib.ptr(h_cols), len(cols), _lib.ptr(h_cpi),
+        float(scale), sum_mode, _lib.ptr(d_sum), _lib.ptr(d_feat) if cols else None,
+        _lib.stream_ptr()), "occx_feature_score")
+    return d_sum, d_feat
+
+
+def feature_score(mixes, ccs, scale: float = 1.0,
+                  table: ThroughputTable = DEFAULT_THROUGHPUT,
+                  sum_mode: int = SUM_MODE) -> FeatureBatch:
+    """K1 over mixes x compute capabilities (ref mix.py:268-352)."""
+    mixes = list(mixes)
+    ccs = list(ccs)
+    cols = [cost_key_of_cc(cc) for cc in ccs]
+    pm = pack_mixes(mixes)
+    d_sum, d_feat = feature_records(_to_device(pm), len(mixes), cols, table.cpi_matrix(),
+                                    scale, sum_mode)
+    sums = _to_host(d_sum, _lib.MIXSUM, len(mixes))
+    feat = _to_host(d_feat, _lib.FEAT, len(mixes) * len(cols)) if cols else np.zeros(0, _lib.FEAT)
+    return FeatureBatch(sums, feat, len(cols), mixes, ccs)
+
+
+# ---------------------------------------------------------------------------
+# K2 + K3: search-space scoring
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class KernelSpec:
+    """One kernel of a search: its tuning space and one InstructionMix per
+    (unroll factor, compiler flag) variant, UIF-major.  Registers / shared
+    memory per candidate come from the space's extra dimensions named
+    ``REGS`` / ``SMEM`` when present, else from these defaults."""
+
+    name: str
+    space: TuningSpace
+    mixes: tuple
+    registers_per_thread: int = 0
+    static_shared_mem: int = 0
+
+    def n_variants(self) -> int:
+        return len(self.space.unroll_factors) * len(self.space.compiler_flags)
+
+
+@dataclass
+class Ranked:
+    """One entry of a segment's top-k list, decoded from its key."""
+
+    index: int              # global candidate index
+    config: tuple           # enumerate_space(kernel.space) tuple
+    variant: int
+    arch: int
+    active_warps: int
+    rule_keep: bool
+    static_keep: bool
+    cost_rank: int | None
+    key: int
+
+
+@dataclass
+class SegmentTopK:
+    kernel: str
+    arch: str
+    entries: list
+
+
+def decode_key(key: int) -> dict:
+    key = int(key)
+    rb = (key >> 34) & 0xFFFFF
+    return {"legal": bool(key >> 63), "rule_keep": bool((key >> 62) & 1),
+            "static_keep": bool((key >> 61) & 1), "active_warps": (key >> 54) & 0x7F,
+            "rank_bits": rb, "index": IDX_MASK - (key & IDX_MASK)}
+
+
+class ScorePlan:
+    """Device-resident tables for scoring a fixed (kernels x archs) search.
+
+    Construction runs K1 (features of every variant on every arch) and the
+    feature-table kernel on the GPU; host work is limited to packing the
+    arch rows, the T* membership masks (tuning.membership_masks) and the
+    Cartesian segment descriptors.  Segment s = kernel * n_arch + arch.
+    """
+
+    def __init__(self, kernels: Sequence[KernelSpec], archs: Sequence[ArchSpec],
+                 mode: Mode = Mode.CORRECTED, k: int = 16,
+                 table: ThroughputTable = DEFAULT_THROUGHPUT, scale: float = 1.0):
+        if not 1 <= k <= 32:
+            raise ValueError("k must be in [1, 32]")
+        self.kernels = list(kernels)
+        self.archs = list(archs)
+        self.mode = Mode(mode)
+        self.k = k
+        self.n_arch = len(self.archs)
+        self.n_seg = len(self.kernels) * self.n_arch
+        self.h_archs = pack_archs(self.archs)
+        # variants
+        mixes, var_kernel, self.var_base = [], [], []
+        for ki, kern in enumerate(self.kernels):
+            if len(kern.mixes) != kern.n_variants():
+                raise ValueError(f"{kern.name}: need one mix per (UIF, CFLAGS) variant")
+            self.var_base.append(len(mixes))
+            mixes += list(kern.mixes)
+            var_kernel += [ki] * len(kern.mixes)
+        self.n_var = len(mixes)
+        # segments: descriptors + value pool + masks
+        pool: list[int] = []
+        desc = np.zeros(self.n_seg, _lib.SEGDESC)
+        masks = np.zeros((self.n_seg, 3), np.uint64)
+        cands = [thread_candidates(a) for a in self.archs]
+        self.seg_start: list[int] = []
+        self.seg_dims: list[list[tuple]] = []
+        start = 0
+        for ki, kern in enumerate(self.kernels):
+            sp = kern.space
+            extras = {name.upper(): vals for name, vals in sp.extra}
+            names = [n.upper() for n, _ in sp.extra]
+            if any(n not in ("REGS", "SMEM") for n in names) or names not in (
+                    [], ["REGS"], ["SMEM"], ["REGS", "SMEM"]):
+                raise ValueError("extra dimensions must be REGS and/or SMEM, in that order")
+            regs = extras.get("REGS", (kern.registers_per_thread,))
+            smem = extras.get("SMEM", (kern.static_shared_mem,))
+            dims = [sp.thread_counts, sp.block_counts, sp.unroll_factors, sp.l1_sizes_kb,
+                    sp.compiler_flags, regs, smem]
+            for vals in (dims[0], dims[1], dims[5], dims[6]):
+                if any((not isinstance(v, int)) or v < 0 for v in vals):
+                    raise ValueError("TC/BC/REGS/SMEM values must be non-negative ints")
+            for a in range(self.n_arch):
+                s = ki * self.n_arch + a
+                size = grid_size(sp)
+                offs, lens = [], []
+                for j, vals in enumerate(dims):
+                    offs.append(len(pool))
+                    lens.append(len(vals))
+                    if j in (0, 1, 5, 6):      # value dims; UIF/PL/CFLAGS by index
+                        pool += [min(int(v), U32_MAX) for v in vals]
+                    else:
+                        pool += [0] * len(vals)
+                desc[s] = (start, size, a, self.var_base[ki], offs, lens)
+                self.seg_start.append(start)
+                self.seg_dims.append([tuple(d) for d in sp._dimensions()])
+                start += size
+                masks[s] = membership_masks(sp, cands[a])
+        self.total = start
+        if self.total > IDX_MASK + 1:
+            raise DeviceError("search space above 2^34 candidates")
+        self.var_kernel = np.asarray(var_kernel, np.uint32)
+        self.mixes = mixes
+        torch = _torch()
+        self.d_desc = _to_device(desc)
+        self.d_pool = _to_device(np.asarray(pool or [0], np.uint32))
+        # K1 on device, then the feature table
+        cols = [int(a["cost_key"]) for a in self.h_archs]
+        d_mix = _to_device(pack_mixes(mixes))
+        self.d_sum, self.d_feat = feature_records(d_mix, self.n_var, cols, table.cpi_matrix(),
+                                                  scale)
+        self.d_vtab = _empty(self.n_var * self.n_arch * _lib.VENT.itemsize)
+        _lib.check(_lib.load().occx_build_vtab(
+            _lib.ctx(), _lib.ptr(self.d_sum), _lib.ptr(self.d_feat), self.n_var, self.n_arch,
+            _lib.ptr(_to_device(self.var_kernel)), _lib.ptr(_to_device(masks)),
+            _lib.ptr(self.d_vtab), _lib.stream_ptr()), "occx_build_vtab")
+        ws = ctypes_u64()
+        _lib.check(_lib.load().occx_score_workspace_bytes(_lib.ctx(), self.n_seg, k,
+                                                          ws.ref()), "workspace")
+        self.ws_bytes = ws.value
+        self.d_ws = _empty(self.ws_bytes)
+        self.masks = masks
+        del torch
+
+    # -- candidates ---------------------------------------------------------
+    def generate(self, begin: int = 0, n: int | None = None, out=None):
+        """Candidates [begin, begin+n) as occx_cand_t records in HBM."""
+        n = self.total - begin if n is None else n
+        out = out if out is not None else _empty(n * 16)
+        _lib.check(_lib.load().occx_gen_space(
+            _lib.ctx(), _lib.ptr(self.d_desc), self.n_seg, _lib.ptr(self.d_pool), begin, n,
+            _lib.ptr(out), _lib.stream_ptr()), "occx_gen_space")
+        return out
+
+    def records_host(self, begin: int = 0, n: int | None = None) -> np.ndarray:
+        n = self.total - begin if n is None else n
+        return _to_host(self.generate(begin, n), _lib.CAND, n)
+
+    # -- scoring ------------------------------------------------------------
+    def score(self, d_records, n: int, index_base: int = 0, out=None, stream=None):
+        """K2+K3 over n records in HBM -> device u64 [n_seg, k] top-k keys."""
+        torch = _torch()
+        out = out if out is not None else torch.zeros((self.n_seg, self.k), dtype=torch.int64,
+                                                       device="cuda")
+        _lib.check(_lib.load().occx_score_topk(
+            _lib.ctx(), _lib.ptr(self.h_archs), self.n_arch, _lib.ptr(d_records), n, index_base,
+            MODE_CODE[self.mode], _lib.ptr(self.d_vtab), self.n_var, self.n_seg, self.k,
+            _lib.ptr(self.d_ws), self.ws_bytes, _lib.ptr(out), _lib.stream_ptr(stream)),
+            "occx_score_topk")
+        return out
+
+    def score_partials(self, d_records, n: int, index_base: int = 0, stream=None):
+        """K2 only: per-CTA tables left in the workspace (timing / custom merges)."""
+        _lib.check(_lib.load().occx_score_topk(
+            _lib.ctx(), _lib.ptr(self.h_archs), self.n_arch, _lib.ptr(d_records), n, index_base,
+            MODE_CODE[self.mode], _lib.ptr(self.d_vtab), self.n_var, self.n_seg, self.k,
+            _lib.ptr(self.d_ws), self.ws_bytes, None, _lib.stream_ptr(stream)),
+            "occx_score_topk")
+        return self.d_ws
+
+    def score_host(self, host, n: int, index_base: int = 0, chunk: int = 1 << 24):
+        """Score n records held in pinned host memory (uint8 tensor, 16 B
+        each): chunked H2D on a copy stream, double-buffered against K2 on
+        the current stream; per-chunk tables merged by K3.  Returns the
+        device [n_seg, k] table (stream-ordered on the current stream)."""
+        torch = _torch()
+        cur = torch.cuda.current_stream()
+        if getattr(self, "_copy_stream", None) is None:
+            self._copy_stream = torch.cuda.Stream()
+        if getattr(self, "_stage", None) is None or self._stage[0].numel() < chunk * 16:
+            self._stage = [_empty(chunk * 16), _empty(chunk * 16)]
+        n_chunks = max(1, -(-n // chunk))
+        tables = torch.zeros((n_chunks, self.n_seg, self.k), dtype=torch.int64, device="cuda")
+        freed = [None, None]
+        for i in range(n_chunks):
+            b = i * chunk
+            m = min(chunk, n - b)
+            if m <= 0:
+                break
+            buf = self._stage[i % 2]
+            with torch.cuda.stream(self._copy_stream):
+                if freed[i % 2] is not None:
+                    self._copy_stream.wait_event(freed[i % 2])
+                buf[: m * 16].copy_(host[b * 16:(b + m) * 16], non_blocking=True)
+                ready = self._copy_stream.record_event()
+            cur.wait_event(ready)
+            self.score(buf, m, index_base=index_base + b, out=tables[i], stream=cur)
+            freed[i % 2] = cur.record_event()
+        if n_chunks == 1:
+            return tables[0]
+        return self.merge(tables, n_chunks)
+
+    def merge(self, d_lists, n_lists: int, out=None, stream=None):
+        """K3 over [n_lists, n_seg, k] device tables -> [n_seg, k]."""
+        torch = _torch()
+        out = out if out is not None else torch.zeros((self.n_seg, self.k), dtype=torch.int64,
+                                                       device="cuda")
+        _lib.check(_lib.load().occx_topk_merge(
+            _lib.ctx(), _lib.ptr(d_lists), n_lists, self.n_seg, self.k, _lib.ptr(out),
+            _lib.stream_ptr(stream)), "occx_topk_merge")
+        return out
+
+    # -- decoding -----------------------------------------------------------
+    def locate(self, gidx: int) -> tuple[int, tuple]:
+        """Global index -> (segment, enumerate_space tuple of its kernel)."""
+        s = bisect.bisect_right(self.seg_start, gidx) - 1
+        local = gidx - self.seg_start[s]
+        dims = self.seg_dims[s]
+        digits = []
+        for vals in reversed(dims):
+            local, r = divmod(local, len(vals))
+            digits.append(vals[r])
+        return s, tuple(reversed(digits))
+
+    def decode(self, keys) -> list[SegmentTopK]:
+        keys = np.asarray(keys.cpu().numpy() if hasattr(keys, "cpu") else keys).view(np.uint64)
+        keys = keys.reshape(self.n_seg, self.k)
+        out = []
+        for s in range(self.n_seg):
+            ki, a = divmod(s, self.n_arch)
+            entries = []
+            for key in keys[s]:
+                key = int(key)
+                if key == 0:
+                    continue
+                d = decode_key(key)
+                seg, cfg = self.locate(d["index"])
+                kern = self.kernels[ki]
+                sp = kern.space
+                i_u = sp.unroll_factors.index(cfg[2])
+                i_c = sp.compiler_flags.index(cfg[4])
+                entries.append(Ranked(
+                    index=d["index"], config=cfg,
+                    variant=self.var_base[ki] + i_u * len(sp.compiler_flags) + i_c,
+                    arch=a, active_warps=d["active_warps"], rule_keep=d["rule_keep"],
+                    static_keep=d["static_keep"],
+                    cost_rank=((1 << 20) - 1 - d["rank_bits"]) if d["rank_bits"] else None,
+                    key=key))
+            out.append(SegmentTopK(self.kernels[ki].name, self.archs[a].name, entries))
+        return out
+
+
+class ctypes_u64:
+    def __init__(self):
+        import ctypes
+        self._v = ctypes.c_uint64(0)
+        self._ctypes = ctypes
+
+    def ref(self):
+        return self._ctypes.byref(self._v)
+
+    @property
+    def value(self) -> int:
+        return int(self._v.value)
+
+
+def score_space(kernels: Sequence[KernelSpec], archs: Sequence[ArchSpec],
+                mode: Mode = Mode.CORRECTED, k: int = 16,
+                chunk: int = 1 << 27) -> list[SegmentTopK]:
+    """Score every candidate of the kernels' spaces on every arch; return
+    the top-k configurations per (kernel, arch).  Candidates are decoded on
+    the device chunk by chunk (chunk x 16 B of HBM) and scored by K2; the
+    per-chunk tables are merged by K3."""
+    torch = _torch()
+    plan = ScorePlan(kernels, archs, mode, k)
+    tables = []
+    buf = _empty(min(chunk, plan.total) * 16)
+    for begin in range(0, plan.total, chunk):
+        n = min(chunk, plan.total - begin)
+        plan.generate(begin, n, out=buf)
+        tables.append(plan.score(buf, n, index_base=begin))
+    if len(tables) == 1:
+        keys = tables[0]
+    else:
+        keys = plan.merge(torch.stack(tables), len(tables))
+    return plan.decode(keys)

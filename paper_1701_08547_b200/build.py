@@ -1,0 +1,63 @@
+"""Build liboccx.so for sm_100a, in-tree (python -m paper_1701_08547_b200.build).
+
+nvcc cross-compiles without a GPU.  Flags: -gencode arch=compute_100a,
+code=sm_100a -lineinfo -O3; the feature kernel is compiled with
+-fmad=false so no multiply-add contraction changes a rounding step
+(DESIGN.md §5).  Object files are cached by source mtime.
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "liboccx.so")
+BUILD = os.path.join(HERE, "_objs")
+NVCC = os.environ.get("NVCC", "nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+SOURCES = {
+    "occx_capi.cu": [],
+    "occx_score.cu": [],
+    "occx_mix.cu": [],
+    "occx_feat.cu": ["-fmad=false"],
+}
+
+
+def _stale(obj: str, deps: list[str]) -> bool:
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(verbose: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    header_deps = [os.path.join(CSRC, "occx_common.cuh"),
+                   os.path.join(os.path.dirname(HERE), "include", "occx.h"), __file__]
+    objs = []
+    for src, extra in SOURCES.items():
+        path = os.path.join(CSRC, src)
+        obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+        objs.append(obj)
+        if _stale(obj, [path] + header_deps):
+            cmd = [NVCC, *ARCH, *COMMON, *extra, "-c", path, "-o", obj]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if verbose or r.returncode:
+                sys.stderr.write(r.stdout + r.stderr)
+            if r.returncode:
+                raise RuntimeError(f"nvcc failed on {src}")
+    if _stale(OUT, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("link of liboccx.so failed")
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv))

@@ -1,0 +1,79 @@
+"""Multi-GPU sharding of a search space.
+
+The candidate space shards by global index: rank g of G scores the
+contiguous range ``shard_range(total, g, G)`` (records decoded on its own
+device, no data-path collective).  The only exchange is one all-gather of
+the fixed-size per-rank top-k table ``[n_seg, k]`` u64 (5 KB for the
+benchmark configs) followed by the K3 merge on every rank.  Because every
+key embeds its candidate's global index, the merged table is identical for
+any G (tests/test_dist.py checks G = 1, 2 with gloo on CPU; the GPU path
+runs the same code with NCCL over NVLink).
+"""
+
+from __future__ import annotations
+
+from typing import Callable
+
+
+def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
+    """[begin, end) of rank's contiguous shard; sizes differ by at most one."""
+    if not 0 <= rank < world:
+        raise ValueError("rank out of range")
+    base, extra = divmod(total, world)
+    begin = rank * base + min(rank, extra)
+    return begin, begin + base + (1 if rank < extra else 0)
+
+
+def allgather_merge(local_table, merge: Callable, group=None):
+    """All-gather every rank's [n_seg, k] table and merge them.
+
+    ``local_table`` is a torch int64 tensor (u64 keys bit-cast); ``merge``
+    maps a stacked [world, n_seg, k] tensor to [n_seg, k] (ScorePlan.merge
+    on the GPU).  One collective, fixed size, latency-bound.
+    """
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    if world == 1:
+        return local_table
+    gathered = torch.empty((world, *local_table.shape), dtype=local_table.dtype,
+                           device=local_table.device)
+    dist.all_gather_into_tensor(gathered, local_table.contiguous(), group=group)
+    return merge(gathered)
+
+
+def score_space_sharded(plan, group=None, chunk: int = 1 << 28, records=None,
+                        stream=None):
+    """Score the plan's whole space across the ranks of ``group``; every
+    rank returns the merged [n_seg, k] device table.
+
+    ``records``: optional pre-generated device records of this rank's shard
+    (the benchmark generates them once, untimed); otherwise the shard is
+    decoded on the device chunk by chunk.
+    """
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    begin, end = shard_range(plan.total, rank, world)
+    n = end - begin
+    if records is not None:
+        local = plan.score(records, n, index_base=begin, stream=stream)
+    else:
+        tables = []
+        buf = None
+        for b in range(begin, end, chunk):
+            m = min(chunk, end - b)
+            if buf is None:
+                buf = torch.empty(m * 16, dtype=torch.uint8, device="cuda")
+            plan.generate(b, m, out=buf)
+            tables.append(plan.score(buf, m, index_base=b, stream=stream))
+        if not tables:
+            local = torch.zeros((plan.n_seg, plan.k), dtype=torch.int64, device="cuda")
+        elif len(tables) == 1:
+            local = tables[0]
+        else:
+            local = plan.merge(torch.stack(tables), len(tables), stream=stream)
+    if world == 1:
+        return local
+    return allgather_merge(local, lambda g: plan.merge(g, g.shape[0], stream=stream), group)

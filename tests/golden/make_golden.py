@@ -1,0 +1,318 @@
+"""Generate the golden fixtures in tests/golden/ FROM THE REFERENCE ITSELF.
+
+Run in the build container (the reference is not on the GPU box):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py [--big]
+
+Imports occmix read-only from /root/reference/pkg/src and records, tagged
+with sys.version (CPython's float sum() changed in 3.12):
+  occupancy_tables.npz   exhaustive limit tables (5 archs x 2 modes):
+                         limit_by_warps T 1..1100, limit_by_registers T x R
+                         (T 1..1100, R 0..300), limit_by_smem S 0..Smax+64
+  occupancy_random.npz   200k random occupancy() calls, every field
+  suggest.json           suggest() over archs x regs x smem x modes
+  mix.json               ATAX fixture aggregate, workload variant features,
+                         3000 random mixes (cost/intensity/shares as hex)
+  corpus.json            aggregate() of the reference parser over the first
+                         2000 kernels of the config-3 corpus text
+  topk_config{1,2,4}.json (and 5 with --big): per-segment top-16 keys of
+                         the scoring composition, computed from reference
+                         functions (limit tables, static/rule_prune,
+                         cost_estimate, intensity)
+The workload *inputs* come from paper_1701_08547_b200.workloads.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import math
+import os
+import random
+import sys
+import time
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, REF)
+sys.dont_write_bytecode = True
+
+import occmix as R  # noqa: E402  (the reference)
+from occmix import mix as Rmix  # noqa: E402
+Rocc = sys.modules["occmix.occupancy"]
+
+from paper_1701_08547_b200 import workloads as W  # noqa: E402
+
+
+def ref_arch(spec):
+    """Reference ArchSpec with the same field values."""
+    if spec.family.value in ("fermi", "kepler", "maxwell", "pascal") and \
+            spec.name == R.builtin_arch(spec.family.value).name:
+        return R.builtin_arch(spec.family.value)
+    return R.arch.parse_arch_config(W.SM100_INI)[0]
+
+
+ARCHS = [ref_arch(a) for a in W.all_archs()]
+MODES = (R.Mode.CORRECTED, R.Mode.VERBATIM)
+META = {"python": sys.version.split()[0], "sum": "neumaier" if sys.version_info >= (3, 12)
+        else "naive", "generator": "tests/golden/make_golden.py"}
+
+
+def _call(f, *a):
+    try:
+        return f(*a)
+    except R.IllegalLaunchError:
+        return -1
+
+
+def occupancy_tables():
+    out = {}
+    for ai, A in enumerate(ARCHS):
+        for mi, m in enumerate(MODES):
+            lw = np.array([_call(R.limit_by_warps, A, t) for t in range(1, 1101)], np.int64)
+            lr = np.array([[_call(R.limit_by_registers, A, t, r, m) for r in range(301)]
+                           for t in range(1, 1101)], np.int64)
+            ls = np.array([R.limit_by_smem(A, s, m)
+                           for s in range(A.shared_mem_per_block + 65)], np.int64)
+            rwl = np.array([Rocc.register_warp_limit(A, r) for r in range(301)], np.int64)
+            out[f"lw_{ai}_{mi}"] = lw
+            out[f"lr_{ai}_{mi}"] = lr
+            out[f"ls_{ai}_{mi}"] = ls
+            out[f"rwl_{ai}_{mi}"] = rwl
+    np.savez_compressed(os.path.join(HERE, "occupancy_tables.npz"), **out)
+
+
+def occupancy_random(n=200_000):
+    rng = random.Random(0x1701)
+    rows = []
+    for _ in range(n):
+        ai = rng.randrange(len(ARCHS))
+        A = ARCHS[ai]
+        mi = rng.randrange(2)
+        t = rng.randrange(0, 1101)
+        r = rng.randrange(0, 301) if rng.random() < 0.9 else rng.randrange(0, 70000)
+        s = rng.randrange(0, A.shared_mem_per_block + 100) if rng.random() < 0.9 \
+            else rng.randrange(0, 1 << 33)
+        try:
+            res = R.occupancy(A, R.LaunchInput(t, r, s), MODES[mi])
+            rows.append((ai, mi, t, r, s, 0, res.warps_per_block, res.limit_warps,
+                         res.limit_regs, res.limit_smem, res.active_blocks, res.active_warps,
+                         ("warps", "registers", "shared-memory", "illegal").index(
+                             res.limiter.value),
+                         np.float64(res.occupancy).view(np.int64)))
+        except R.IllegalLaunchError:
+            rows.append((ai, mi, t, r, s, 1, 0, 0, 0, 0, 0, 0, 3, 0))
+    arr = np.array(rows, np.int64)
+    np.savez_compressed(os.path.join(HERE, "occupancy_random.npz"), rows=arr)
+
+
+def suggest_golden():
+    rows = []
+    for ai, A in enumerate(ARCHS):
+        for mi, m in enumerate(MODES):
+            for regs in list(range(0, 256, 3)) + [255, 256, 63, 64]:
+                for smem in (0, 1, 4096, 6144, 6145, 10000, 12288, 24576, 49152, 49153,
+                             232448, 232449):
+                    res = R.KernelResources("k", registers_per_thread=regs,
+                                            static_shared_mem=smem)
+                    try:
+                        s = R.suggest(A, res, m)
+                        rows.append([ai, mi, regs, smem, "ok", list(s.thread_candidates),
+                                     s.register_headroom, s.smem_budget,
+                                     s.best_occupancy.hex(), s.best_threads, s.best_blocks])
+                    except R.IllegalLaunchError:
+                        rows.append([ai, mi, regs, smem, "illegal"])
+    with open(os.path.join(HERE, "suggest.json"), "w") as fh:
+        json.dump({"meta": META, "rows": rows}, fh)
+
+
+def _ref_mix(counts_pairs, regs):
+    return R.InstructionMix({R.OpClass(c.value if hasattr(c, "value") else c): n
+                             for c, n in counts_pairs}, regs)
+
+
+def _features(mx, cc):
+    try:
+        return {"cost": R.cost_estimate(mx, cc).hex(),
+                "cycles": [v.hex() for v in Rmix.category_cycles(mx, cc).values()],
+                "coef": [v.hex() for v in Rmix.category_coefficients(mx, cc).values()],
+                "shares": [v.hex() for v in R.pipeline_utilization(mx, cc).values()],
+                "per_class": {c.value: v.hex() for c, v in
+                              Rmix.per_class_cycles(mx, cc).items()}}
+    except R.UnsupportedArchitectureError:
+        return "unsupported"
+
+
+def mix_golden():
+    sass = open("/root/reference/pkg/tests/data/atax_kepler.sass.txt").read()
+    ((name, instrs),) = R.parse_disassembly(sass)
+    mx = R.aggregate(instrs)
+    atax = {"name": name, "counts": [[c.value, n] for c, n in mx.counts.items()],
+            "reg_operands": mx.reg_operands, "flops": mx.flops, "mem": mx.mem,
+            "ctrl": mx.ctrl, "total": mx.total_instructions,
+            "intensity": R.intensity(mx).hex(),
+            "instructions": [[i.opcode, list(i.modifiers), i.predicate,
+                              i.register_operand_count] for i in instrs],
+            "features": {str(cc): _features(mx, cc) for cc in (2.0, 3.5, 5.2, 6.0, 10.0)}}
+    variants = []
+    for kname in W.KERNEL_NAMES:
+        for u in range(1, 6):
+            for f in ("", "-use_fast_math"):
+                vm = W.variant_mix(kname, u, f)
+                rm = _ref_mix(list(vm.counts.items()), vm.reg_operands)
+                variants.append({"kernel": kname, "unroll": u, "flag": f,
+                                 "counts": [[c.value, n] for c, n in rm.counts.items()],
+                                 "reg_operands": rm.reg_operands,
+                                 "intensity": R.intensity(rm).hex(),
+                                 "features": {str(cc): _features(rm, cc)
+                                              for cc in (2.0, 3.5, 5.2, 6.0, 10.0)}})
+    rng = random.Random(0xFEED)
+    classes = [c for c in R.OpClass if c is not R.OpClass.REGS]
+    rand = []
+    for i in range(3000):
+        k = rng.randrange(0, 9)
+        picked = rng.sample(classes, k)
+        counts = [[c.value, rng.choice((0, 1, 2, 3, 7, 13, 100, 999, 123457))
+                   if rng.random() < 0.2 else rng.randrange(0, 600)] for c in picked]
+        regs = rng.randrange(0, 5000)
+        rm = R.InstructionMix({R.OpClass(c): n for c, n in counts}, regs)
+        scale = rng.choice((1.0, 0.5, 3.0, 1e-3, 7.25))
+        cc = rng.choice((2.0, 3.5, 5.2, 6.0))
+        rand.append({"counts": counts, "reg_operands": regs, "scale": scale.hex(), "cc": cc,
+                     "cost_scaled": R.cost_estimate(rm, cc, scale).hex(),
+                     "intensity": R.intensity(rm).hex(), "features": _features(rm, cc)})
+    with open(os.path.join(HERE, "mix.json"), "w") as fh:
+        json.dump({"meta": META, "atax": atax, "variants": variants, "random": rand}, fh)
+
+
+def corpus_golden(n_kernels=2000):
+    c = W.make_corpus(n_kernels)
+    text = W.corpus_text(c)
+    t0 = time.time()
+    funcs = R.parse_disassembly(text)
+    rows = []
+    for name, instrs in funcs:
+        mx = R.aggregate(instrs)
+        rows.append([name, [[cl.value, n] for cl, n in mx.counts.items()], mx.reg_operands])
+    with open(os.path.join(HERE, "corpus.json"), "w") as fh:
+        json.dump({"meta": META, "n_kernels": n_kernels, "n_instr": c.n_instr,
+                   "text_sha256": hashlib.sha256(text.encode()).hexdigest(),
+                   "reference_seconds": time.time() - t0, "kernels": rows}, fh)
+
+
+# ---------------------------------------------------------------------------
+# scoring composition from reference functions (B1: separable tables)
+# ---------------------------------------------------------------------------
+
+IDX = (1 << 34) - 1
+
+
+def _segment_tables(A, mode, tcs, regs, smem):
+    lw = np.array([_call(R.limit_by_warps, A, t) for t in tcs], np.int64)
+    lr = np.array([[_call(R.limit_by_registers, A, t, r, mode) for r in regs] for t in tcs],
+                  np.int64)
+    ls = np.array([R.limit_by_smem(A, s, mode) for s in smem], np.int64)
+    wpb = np.array([Rocc.warps_per_block(A, t) for t in tcs], np.int64)
+    return lw, lr, ls, wpb
+
+
+def topk_config(cfg, mode=R.Mode.CORRECTED, verbose=True):
+    """Per-segment top-k keys for a workloads.Config, via reference calls."""
+    archs = [ref_arch(a) for a in cfg.archs]
+    n_arch = len(archs)
+    out = []
+    start = 0
+    for ki, kern in enumerate(cfg.kernels):
+        sp = kern.space
+        extras = dict(sp.extra)
+        regs = extras.get("REGS", (kern.registers_per_thread,))
+        smem = extras.get("SMEM", (kern.static_shared_mem,))
+        rspace = R.TuningSpace(sp.thread_counts, sp.block_counts, sp.unroll_factors,
+                               sp.l1_sizes_kb, sp.compiler_flags, sp.extra)
+        size = R.grid_size(rspace)
+        rmixes = [_ref_mix(list(m.counts.items()), m.reg_operands) for m in kern.mixes]
+        for a, A in enumerate(archs):
+            t0 = time.time()
+            sugg = R.suggest(A, R.KernelResources("k"))
+            try:
+                st = set(R.static_prune(rspace, sugg).kept_thread_counts)
+                lo = set(R.rule_prune(rspace, sugg, 0.0).kept_thread_counts)
+                hi = set(R.rule_prune(rspace, sugg, math.inf).kept_thread_counts)
+            except R.NoCandidatesError:
+                st, lo, hi = set(), set(), set()
+            try:
+                costs = [R.cost_estimate(m, A.compute_capability) for m in rmixes]
+                distinct = sorted(set(costs))
+                rank_bits = [(1 << 20) - 1 - distinct.index(c) for c in costs]
+            except R.UnsupportedArchitectureError:
+                rank_bits = [0] * len(rmixes)
+            upper = [R.intensity(m) > 4.0 for m in rmixes]
+            lw, lr, ls, wpb = _segment_tables(A, mode, sp.thread_counts, regs, smem)
+            nT, nB, nU, nP, nF = (len(sp.thread_counts), len(sp.block_counts),
+                                  len(sp.unroll_factors), len(sp.l1_sizes_kb),
+                                  len(sp.compiler_flags))
+            nR, nS = len(regs), len(smem)
+            best = np.zeros(0, np.uint64)
+            for it, t in enumerate(sp.thread_counts):
+                if lw[it] < 0:
+                    continue
+                # (B, U, P, F, R, S) block for this T, vectorised
+                blocks = np.minimum(np.minimum(lw[it], lr[it][:, None]), ls[None, :])  # R x S
+                aw = np.minimum(blocks * wpb[it], A.max_warps_per_mp)
+                legal = blocks > 0
+                var = (np.arange(nU)[:, None] * nF + np.arange(nF)[None, :]).reshape(-1)
+                rb = np.array(rank_bits, np.uint64)[var]                      # U*F
+                ru = np.array([(t in (hi if upper[v] else lo)) for v in var], np.uint64)
+                stb = np.uint64(1 if t in st else 0)
+                hi_bits = (np.uint64(1) << np.uint64(63)) | (ru << np.uint64(62)) | \
+                    (stb << np.uint64(61)) | (rb << np.uint64(34))           # U*F
+                hb = np.broadcast_to(hi_bits.reshape(1, nU, 1, nF), (nB, nU, nP, nF))
+                key_hi = hb[..., None, None] | \
+                    (aw.astype(np.uint64) << np.uint64(54))[None, None, None, None]
+                local = (np.arange(nB * nU * nP * nF * nR * nS, dtype=np.int64)
+                         .reshape(nB, nU, nP, nF, nR, nS) + it * nB * nU * nP * nF * nR * nS)
+                gidx = (start + local).astype(np.uint64)
+                keys = key_hi | (np.uint64(IDX) - gidx)
+                keys = np.where(np.broadcast_to(legal, keys.shape), keys, np.uint64(0))
+                flat = keys.reshape(-1)
+                if flat.size > 64:
+                    part = flat[np.argpartition(flat, flat.size - 16)[-16:]]
+                else:
+                    part = flat
+                best = np.concatenate([best, part])
+                best = np.sort(best)[::-1][:16]
+            best = np.concatenate([best, np.zeros(16 - len(best), np.uint64)])
+            out.append([int(x) for x in best[:cfg.k]])
+            start += size
+            if verbose:
+                print(f"  seg k={ki} a={a}: {size} candidates, {time.time() - t0:.1f}s",
+                      flush=True)
+    return out
+
+
+def topk_golden(name):
+    cfg = W.CONFIGS[name]()
+    t0 = time.time()
+    res = {"meta": META, "config": cfg.name, "total": cfg.total,
+           "corrected": topk_config(cfg, R.Mode.CORRECTED)}
+    if name in ("config1", "config2"):
+        res["verbatim"] = topk_config(cfg, R.Mode.VERBATIM)
+    res["seconds"] = time.time() - t0
+    with open(os.path.join(HERE, f"topk_{name}.json"), "w") as fh:
+        json.dump(res, fh)
+
+
+if __name__ == "__main__":
+    steps = sys.argv[1:] or ["tables", "random", "suggest", "mix", "corpus", "config1",
+                             "config2", "config4"]
+    if "--big" in steps:
+        steps = [s for s in steps if s != "--big"] + ["config5"]
+    for s in steps:
+        t0 = time.time()
+        {"tables": occupancy_tables, "random": occupancy_random, "suggest": suggest_golden,
+         "mix": mix_golden, "corpus": corpus_golden}.get(s, lambda: topk_golden(s))()
+        print(f"{s}: {time.time() - t0:.1f}s", flush=True)

@@ -1,0 +1,325 @@
+"""GPU parity: every kernel of liboccx.so against the reference goldens and
+the oracle, through the C ABI (ctypes).  Run on a B200: pytest -m gpu."""
+
+import hashlib
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import pyref
+from helpers import problem_of, same_sum_semantics, spaces_of
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    assert t.cuda.is_available()
+    return t
+
+
+@pytest.fixture(scope="module")
+def P(torch):
+    import paper_1701_08547_b200 as p
+    from paper_1701_08547_b200 import _lib
+    _lib.load()
+    return p
+
+
+# ---------------------------------------------------------------------------
+# Kd: occupancy dump
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("ai", range(5))
+@pytest.mark.parametrize("mode", ["corrected", "verbatim"])
+def test_kd_exhaustive_limit_tables(P, golden, archs, ai, mode):
+    from paper_1701_08547_b200.batch import occupancy_batch
+    g = golden("occupancy_tables.npz")
+    mi = 0 if mode == "corrected" else 1
+    A = archs[ai]
+    T = np.repeat(np.arange(1, 1101), 301)
+    R = np.tile(np.arange(301), 1100)
+    ob = occupancy_batch(A, np.stack([T, R, np.zeros_like(T)], 1), mode)
+    legal = ob.raw["status"] == 0
+    lw = np.where(legal, ob.raw["limit_warps"], -1).reshape(1100, 301)[:, 0]
+    lr = np.where(legal, ob.raw["limit_regs"].astype(np.int64), -1).reshape(1100, 301)
+    np.testing.assert_array_equal(lw, g[f"lw_{ai}_{mi}"])
+    np.testing.assert_array_equal(lr, g[f"lr_{ai}_{mi}"])
+    np.testing.assert_array_equal(ob.raw["reg_warp_limit"].reshape(1100, 301)[0],
+                                  g[f"rwl_{ai}_{mi}"])
+    S = np.arange(A.shared_mem_per_block + 65)
+    ob = occupancy_batch(A, np.stack([np.full_like(S, 32), np.zeros_like(S), S], 1), mode)
+    np.testing.assert_array_equal(ob.raw["limit_smem"], g[f"ls_{ai}_{mi}"])
+
+
+def test_kd_random_all_fields(P, golden, archs):
+    from paper_1701_08547_b200.batch import occupancy_batch
+    rows = golden("occupancy_random.npz")["rows"]
+    for mi, mode in enumerate(("corrected", "verbatim")):
+        sel = rows[rows[:, 1] == mi]
+        ob = occupancy_batch(archs, sel[:, 2:5], mode, arch_index=sel[:, 0])
+        r = ob.raw
+        illegal = sel[:, 5] == 1
+        np.testing.assert_array_equal(r["status"] == 2, illegal)
+        got = np.stack([r["wpb"], r["limit_warps"], r["limit_regs"], r["limit_smem"],
+                        r["active_blocks"], r["active_warps"], r["limiter"],
+                        r["occupancy"].view(np.int64)], 1).astype(np.int64)
+        np.testing.assert_array_equal(got[~illegal], sel[~illegal][:, 6:14])
+
+
+# ---------------------------------------------------------------------------
+# K4: suggest
+# ---------------------------------------------------------------------------
+
+def test_k4_suggest_golden(P, golden, archs):
+    from paper_1701_08547_b200.batch import suggest_batch
+    rows = golden("suggest.json")["rows"]
+    for mi, mode in enumerate(("corrected", "verbatim")):
+        ok = [r for r in rows if r[1] == mi and r[4] == "ok"]
+        reqs = [(archs[r[0]], P.KernelResources("k", r[2], r[3])) for r in ok]
+        got = suggest_batch(reqs, mode)
+        for r, s in zip(ok, got):
+            assert [list(s.thread_candidates), s.register_headroom, s.smem_budget,
+                    s.best_occupancy.hex(), s.best_threads, s.best_blocks] == r[5:], r
+        for r in rows:
+            if r[1] == mi and r[4] == "illegal":
+                with pytest.raises(P.IllegalLaunchError):
+                    suggest_batch([(archs[r[0]], P.KernelResources("k", r[2], r[3]))], mode)
+
+
+# ---------------------------------------------------------------------------
+# K1: features
+# ---------------------------------------------------------------------------
+
+def _mix(P, pairs, regs):
+    return P.InstructionMix({P.OpClass(c): n for c, n in pairs}, regs)
+
+
+def test_k1_features_golden(P, golden):
+    from paper_1701_08547_b200.batch import feature_score
+    g = golden("mix.json")
+    if not same_sum_semantics(g["meta"]):
+        pytest.skip("goldens captured under a different CPython sum()")
+    ccs = [2.0, 3.5, 5.2, 6.0, 10.0]
+    items = g["variants"] + [g["atax"]]
+    mixes = [_mix(P, v["counts"], v["reg_operands"]) for v in items]
+    fb = feature_score(mixes, ccs)
+    for m, v in enumerate(items):
+        assert fb.intensity[m].hex() == v["intensity"]
+        for j, cc in enumerate(ccs):
+            f = v["features"][str(cc)]
+            if f == "unsupported":
+                with pytest.raises(P.UnsupportedArchitectureError):
+                    fb.one(m, j)
+                continue
+            got = fb.one(m, j)
+            assert got.cost.hex() == f["cost"]
+            assert [x.hex() for x in got.cycles.values()] == f["cycles"]
+            assert [x.hex() for x in got.coefficients.values()] == f["coef"]
+            assert [x.hex() for x in got.shares.values()] == f["shares"]
+            assert {c.value: x.hex() for c, x in got.per_class.items()} == f["per_class"]
+
+
+def test_k1_random_mixes_golden(P, golden):
+    from paper_1701_08547_b200.batch import feature_score
+    g = golden("mix.json")
+    if not same_sum_semantics(g["meta"]):
+        pytest.skip("goldens captured under a different CPython sum()")
+    by_key = {}
+    for i, v in enumerate(g["random"]):
+        by_key.setdefault((v["cc"], v["scale"]), []).append(i)
+    for (cc, scale), idx in by_key.items():
+        mixes = [_mix(P, g["random"][i]["counts"], g["random"][i]["reg_operands"]) for i in idx]
+        fb = feature_score(mixes, [cc], scale=float.fromhex(scale))
+        for m, i in enumerate(idx):
+            v = g["random"][i]
+            assert fb.one(m, 0).cost.hex() == v["cost_scaled"]
+            assert fb.intensity[m].hex() == v["intensity"]
+
+
+# ---------------------------------------------------------------------------
+# K0: aggregate
+# ---------------------------------------------------------------------------
+
+class _Ins:
+    def __init__(self, opcode, mods, pred, nreg):
+        self.opcode, self.modifiers, self.predicate = opcode, tuple(mods), pred
+        self.register_operand_count = nreg
+
+
+def test_k0_atax_fixture(P, golden):
+    a = golden("mix.json")["atax"]
+    mx = P.aggregate([_Ins(*i) for i in a["instructions"]])
+    assert [[c.value, n] for c, n in mx.counts.items()] == a["counts"]
+    assert (mx.reg_operands, mx.flops, mx.mem, mx.ctrl, mx.total_instructions) == \
+        (a["reg_operands"], a["flops"], a["mem"], a["ctrl"], a["total"])
+
+
+def _k0(P, torch, corpus):
+    from paper_1701_08547_b200 import _lib, batch, workloads
+    rec = workloads.corpus_records(corpus)
+    lut = workloads.corpus_signature_lut()
+    d = batch.mix_reduce(batch._to_device(rec), batch._to_device(corpus.offsets),
+                         corpus.n_kernels, batch._to_device(lut), len(lut))
+    torch.cuda.synchronize()
+    return batch._to_host(d, _lib.MIX, corpus.n_kernels), rec, lut
+
+
+def test_k0_corpus_golden(P, torch, golden):
+    from paper_1701_08547_b200 import workloads
+    from paper_1701_08547_b200.batch import mix_from_record
+    g = golden("corpus.json")
+    c = workloads.make_corpus(g["n_kernels"])
+    assert hashlib.sha256(workloads.corpus_text(c).encode()).hexdigest() == g["text_sha256"]
+    out, _, _ = _k0(P, torch, c)
+    for m, (name, pairs, reg) in zip(out, g["kernels"]):
+        mx = mix_from_record(m)
+        assert [[cl.value, n] for cl, n in mx.counts.items()] == pairs, name
+        assert mx.reg_operands == reg
+
+
+def test_k0_full_corpus_vs_oracle(P, torch):
+    """Config 3 at full size: 100k kernels, ~1e8 instruction records."""
+    from paper_1701_08547_b200 import workloads
+    c = workloads.make_corpus(100_000)
+    out, rec, lut = _k0(P, torch, c)
+    counts, order, regs = oracle.aggregate_records(rec, c.offsets, lut)
+    np.testing.assert_array_equal(out["counts"][:, :15].astype(np.int64), counts)
+    np.testing.assert_array_equal(out["reg_operands"].astype(np.int64), regs)
+    # insertion order: sort present classes by first_key
+    fk = out["first_key"][:, :15].astype(np.int64)
+    fk = np.where(out["counts"][:, :15] > 0, fk, 1 << 40)
+    got_order = np.argsort(fk, axis=1, kind="stable")
+    n_present = (counts > 0).sum(1)
+    mask = np.arange(15)[None, :] < n_present[:, None]
+    np.testing.assert_array_equal(np.where(mask, got_order, -1), order)
+
+
+# ---------------------------------------------------------------------------
+# K2 + K3: scoring
+# ---------------------------------------------------------------------------
+
+def _score_config(P, torch, cfg, mode="corrected", chunk=None):
+    plan = P.ScorePlan(cfg.kernels, cfg.archs, mode, k=cfg.k)
+    if chunk is None:
+        rec = plan.generate()
+        keys = plan.score(rec, plan.total)
+    else:
+        tabs = []
+        for b in range(0, plan.total, chunk):
+            n = min(chunk, plan.total - b)
+            tabs.append(plan.score(plan.generate(b, n), n, index_base=b))
+        keys = plan.merge(torch.stack(tabs), len(tabs))
+    return plan, keys.cpu().numpy().view(np.uint64)
+
+
+@pytest.mark.parametrize("name", ["config1", "config2", "config4"])
+def test_k2_topk_golden(P, torch, golden, name):
+    from paper_1701_08547_b200 import workloads
+    g = golden(f"topk_{name}.json")
+    cfg = workloads.CONFIGS[name]()
+    for mode in ("corrected", "verbatim"):
+        if mode in g:
+            _, keys = _score_config(P, torch, cfg, mode)
+            assert keys.tolist() == g[mode], (name, mode)
+
+
+def test_k2_config5_golden(P, torch, golden):
+    """The 1.28e9-candidate sweep on one GPU, in 4 chunks + K3 merge."""
+    import os
+    from paper_1701_08547_b200 import workloads
+    path = os.path.join(os.path.dirname(__file__), "golden", "topk_config5.json")
+    if not os.path.exists(path):
+        pytest.skip("topk_config5.json not generated")
+    g = golden("topk_config5.json")
+    _, keys = _score_config(P, torch, workloads.config5(), chunk=1 << 29)
+    assert keys.tolist() == g["corrected"]
+
+
+def test_k2_config1_decode(P, torch):
+    from paper_1701_08547_b200 import workloads
+    res = P.score_space(workloads.config1().kernels, workloads.config1().archs)
+    (seg,) = res
+    assert [e.config[0] for e in seg.entries] == [128, 256, 512, 1024, 224, 288, 672, 992,
+                                                  160, 192, 320, 384, 480, 640, 960, 928]
+    assert all(e.config[1:] == (24, 1, 16, "") for e in seg.entries)
+
+
+def test_k2_shuffled_records_vs_oracle(P, torch):
+    """No order exploitation: a seeded permutation of config 2's records."""
+    from paper_1701_08547_b200 import workloads
+    cfg = workloads.config2()
+    plan = P.ScorePlan(cfg.kernels, cfg.archs, k=cfg.k)
+    rec = plan.generate()
+    perm = torch.randperm(plan.total, generator=torch.Generator().manual_seed(7)).cuda()
+    shuf = rec[: plan.total * 16].view(plan.total, 16)[perm].reshape(-1).contiguous()
+    keys = plan.score(shuf, plan.total).cpu().numpy().view(np.uint64)
+    want = oracle.score_records(problem_of(cfg), shuf.cpu().numpy())
+    assert np.array_equal(keys, want)
+
+
+def test_k2_chunked_equals_oneshot(P, torch, golden):
+    from paper_1701_08547_b200 import workloads
+    g = golden("topk_config4.json")
+    _, keys = _score_config(P, torch, workloads.config4(), chunk=12_345_679)
+    assert keys.tolist() == g["corrected"]
+
+
+@pytest.mark.parametrize("k", [1, 5, 16, 32])
+def test_k2_k_values_and_edges(P, torch, k):
+    """k in [1, 32]; odd sizes; illegal / out-of-range records excluded."""
+    from paper_1701_08547_b200 import _lib, batch, workloads
+    from paper_1701_08547_b200.batch import KernelSpec
+    cfg = workloads.config2()
+    kernels = cfg.kernels[:2]
+    plan = P.ScorePlan(kernels, cfg.archs, k=k)
+    n = 1_000_003
+    host = plan.records_host(3_000_000, n)
+    # corrupt some records: bad arch, bad variant, T = 0, T > Tmax, R > Rmax
+    rng = np.random.default_rng(k)
+    idx = rng.choice(n, 5000, replace=False)
+    host["arch"][idx[:1000]] = 200
+    host["variant"][idx[1000:2000]] = 10_000
+    host["threads"][idx[2000:3000]] = 0
+    host["threads"][idx[3000:4000]] = 1056
+    host["regs"][idx[4000:]] = 300
+    d = batch._to_device(host)
+    keys = plan.score(d, n, index_base=3_000_000).cpu().numpy().view(np.uint64)
+    prob = problem_of(cfg, False)
+    prob2 = problem_of(type(cfg)(cfg.name, kernels, cfg.archs, k))
+    want = oracle.score_records(prob2, host, index_base=3_000_000)
+    assert np.array_equal(keys, want)
+    del prob
+
+
+def test_k2_empty_and_tiny(P, torch):
+    from paper_1701_08547_b200 import workloads, batch
+    cfg = workloads.config1()
+    plan = P.ScorePlan(cfg.kernels, cfg.archs, k=16)
+    keys = plan.score(batch._empty(16), 0).cpu().numpy()
+    assert (keys == 0).all()
+    rec = plan.generate(5, 1)
+    keys = plan.score(rec, 1, index_base=5).cpu().numpy().view(np.uint64)
+    assert pyref.key_index(int(keys[0, 0])) == 5 and (keys[0, 1:] == 0).all()
+
+
+def test_k2_many_segments(P, torch):
+    """Hundreds of segments (smem tables scale with n_seg)."""
+    from paper_1701_08547_b200 import workloads
+    from paper_1701_08547_b200.batch import KernelSpec
+    from paper_1701_08547_b200.tuning import TuningSpace
+    ks = []
+    for i in range(60):
+        name = workloads.KERNEL_NAMES[i % 4]
+        space = TuningSpace(tuple(range(32, 1025, 32)), (24, 48), (1, 2), (16,), ("", "-use_fast_math"),
+                            extra=(("REGS", tuple(range(i % 7, 256, 17))), ("SMEM", (0, 4096 * (i % 5)))))
+        ks.append(workloads.kernel_spec(name, space))
+    cfg = workloads.Config("many", tuple(ks), tuple(workloads.all_archs()), 8)
+    plan = P.ScorePlan(cfg.kernels, cfg.archs, k=8)
+    keys = plan.score(plan.generate(), plan.total).cpu().numpy().view(np.uint64)
+    want = oracle.score_spaces(problem_of(cfg), spaces_of(cfg), threads=8)
+    assert plan.n_seg == 300
+    assert np.array_equal(keys, want)
