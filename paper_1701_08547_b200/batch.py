@@ -492,7 +492,7 @@ class ScorePlan:
                         pool += [0] * len(vals)
                 desc[s] = (start, size, a, self.var_base[ki], offs, lens)
                 self.seg_start.append(start)
-                self.seg_dims.append([tuple(d) for d in sp._dimensions()])
+                self.seg_dims.append([tuple(v) for _, v in sp._dimensions()])
                 start += size
                 masks[s] = membership_masks(sp, cands[a])
         self.total = start
@@ -509,9 +509,14 @@ class ScorePlan:
         self.d_sum, self.d_feat = feature_records(d_mix, self.n_var, cols, table.cpi_matrix(),
                                                   scale)
         self.d_vtab = _empty(self.n_var * self.n_arch * _lib.VENT.itemsize)
+        # keep every input tensor referenced until after the launch: a
+        # temporary freed before the call would be recycled by the next
+        # allocation and overwritten before the kernel reads it
+        self.d_var_kernel = _to_device(self.var_kernel)
+        self.d_masks = _to_device(masks)
         _lib.check(_lib.load().occx_build_vtab(
             _lib.ctx(), _lib.ptr(self.d_sum), _lib.ptr(self.d_feat), self.n_var, self.n_arch,
-            _lib.ptr(_to_device(self.var_kernel)), _lib.ptr(_to_device(masks)),
+            _lib.ptr(self.d_var_kernel), _lib.ptr(self.d_masks),
             _lib.ptr(self.d_vtab), _lib.stream_ptr()), "occx_build_vtab")
         ws = ctypes_u64()
         _lib.check(_lib.load().occx_score_workspace_bytes(_lib.ctx(), self.n_seg, k,

@@ -18,7 +18,8 @@ OUT = os.path.join(HERE, "liboccx.so")
 BUILD = os.path.join(HERE, "_objs")
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+          "-cudart", "shared"]
 SOURCES = {
     "occx_capi.cu": [],
     "occx_score.cu": [],
@@ -51,7 +52,7 @@ def build(verbose: bool = False) -> str:
             if r.returncode:
                 raise RuntimeError(f"nvcc failed on {src}")
     if _stale(OUT, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart"]
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", OUT, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             sys.stderr.write(r.stdout + r.stderr)

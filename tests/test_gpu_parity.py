@@ -44,7 +44,7 @@ def test_kd_exhaustive_limit_tables(P, golden, archs, ai, mode):
     R = np.tile(np.arange(301), 1100)
     ob = occupancy_batch(A, np.stack([T, R, np.zeros_like(T)], 1), mode)
     legal = ob.raw["status"] == 0
-    lw = np.where(legal, ob.raw["limit_warps"], -1).reshape(1100, 301)[:, 0]
+    lw = np.where(legal, ob.raw["limit_warps"].astype(np.int64), -1).reshape(1100, 301)[:, 0]
     lr = np.where(legal, ob.raw["limit_regs"].astype(np.int64), -1).reshape(1100, 301)
     np.testing.assert_array_equal(lw, g[f"lw_{ai}_{mi}"])
     np.testing.assert_array_equal(lr, g[f"lr_{ai}_{mi}"])
