@@ -134,8 +134,10 @@ typedef struct occx_feat_t {
  * column (mix.py:99-106 raises).                                         */
 typedef struct occx_vent_t {
   uint32_t member[4];
-  uint32_t seg, rank_bits;
-  uint32_t reserved[2];
+  uint32_t seg;
+  uint32_t key_hi;        /* 0x80000000 | rank_bits << 2: key bits 63, 53-34 */
+  uint32_t rank_bits;
+  uint32_t reserved;
 } occx_vent_t;
 
 /* Cartesian segment of a TuningSpace (tuning.py:30-77) for the on-device

@@ -36,8 +36,8 @@ MIXSUM = np.dtype([("intensity", "<f8"), ("flops", "<u8"), ("mem", "<u8"),
 FEAT = np.dtype([("cost", "<f8"), ("coef", "<f8", 4), ("cycles", "<f8", 4),
                  ("shares", "<f8", 4), ("per_class", "<f8", 16),
                  ("status", "<i4"), ("reserved", "<i4")])
-VENT = np.dtype([("member", "<u4", 4), ("seg", "<u4"), ("rank_bits", "<u4"),
-                 ("reserved", "<u4", 2)])
+VENT = np.dtype([("member", "<u4", 4), ("seg", "<u4"), ("key_hi", "<u4"),
+                 ("rank_bits", "<u4"), ("reserved", "<u4")])
 SEGDESC = np.dtype([("start", "<u8"), ("size", "<u8"), ("arch", "<u4"),
                     ("var_base", "<u4"), ("dim_off", "<u4", 7), ("dim_len", "<u4", 7)])
 SUGG_IN = np.dtype([("arch", "<u4"), ("regs", "<u4"), ("smem", "<u4"), ("reserved", "<u4")])

@@ -37,8 +37,8 @@ def _stale(obj: str, deps: list[str]) -> bool:
 
 def build(verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
-    header_deps = [os.path.join(CSRC, "occx_common.cuh"),
-                   os.path.join(os.path.dirname(HERE), "include", "occx.h"), __file__]
+    header_deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
+    header_deps += [os.path.join(os.path.dirname(HERE), "include", "occx.h"), __file__]
     objs = []
     for src, extra in SOURCES.items():
         path = os.path.join(CSRC, src)

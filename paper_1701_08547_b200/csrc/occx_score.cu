@@ -11,7 +11,9 @@
 // shared-memory compare; survivors are inserted warp-cooperatively under
 // a per-segment shared-memory lock.  K3 merges the per-CTA tables.
 #include <cstdio>
+#include <cstdlib>
 #include "occx_common.cuh"
+#include "occx_k2.cuh"
 
 using namespace occx;
 
@@ -25,7 +27,6 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   return v;
 }
 
-__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 // ---------------------------------------------------------------------------
 // Kd: full OccupancyResult per candidate
@@ -39,7 +40,7 @@ struct DumpParams {
 
 template <int MODE>
 __global__ void __launch_bounds__(256) occ_dump_kernel(const __grid_constant__ DumpParams p) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   SmemArch sa = build_arch_tables<MODE>(p.archs, smem);
   __syncthreads();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -72,7 +73,7 @@ __global__ void __launch_bounds__(256) occ_dump_kernel(const __grid_constant__ D
 }
 
 // ---------------------------------------------------------------------------
-// K2: fused score + CTA-local per-segment top-k
+// K2: fused score + CTA-local per-segment top-k (occx_k2.cuh for the core)
 // ---------------------------------------------------------------------------
 struct ScoreParams {
   ArchParams archs;
@@ -80,35 +81,10 @@ struct ScoreParams {
   uint64_t n;
   uint64_t index_base;
   const occx_vent_t* vtab;
-  uint32_t n_var, n_seg, k, pad;
+  uint32_t n_var, n_seg, k, vt_smem;
   uint64_t chunk;           // candidates per CTA, multiple of the tile
   uint64_t* partials;       // [gridDim.x][n_seg][k]
 };
-
-constexpr int kScoreThreads = 512;
-constexpr int kScoreUnroll = 4;
-
-template <int MODE>
-__device__ __forceinline__ void score_one(const SmemArch& sa, const ScoreParams& p, uint4 r,
-                                          uint64_t gidx, uint64_t& key, uint32_t& seg) {
-  const uint32_t variant = r.x, S = r.y, T = r.z & 0xffffu, R = r.w & 0xffffu,
-                 a = (r.w >> 16) & 0xffu;
-  key = 0;
-  seg = 0;
-  if (a >= (uint32_t)p.archs.n || variant >= p.n_var) return;
-  const uint32_t aw = eval_active_warps<MODE>(sa, a, T, R, S);
-  if (aw == 0) return;                      // illegal launch or zero blocks
-  const occx_vent_t* e = p.vtab + ((size_t)variant * p.archs.n + a);
-  const uint2 sr = __ldg(reinterpret_cast<const uint2*>(&e->seg));
-  const uint32_t b = T >> 5;
-  uint32_t bits = 0;
-  if ((T & 31u) == 0 && b < 64) bits = (__ldg(&e->member[b >> 4]) >> ((b & 15u) * 2)) & 3u;
-  const uint64_t inv = kIdxMask - gidx;
-  const uint32_t hi = 0x80000000u | (bits << 29) | (aw << 22) | (sr.y << 2) |
-                      (uint32_t)(inv >> 32);
-  key = ((uint64_t)hi << 32) | (uint32_t)inv;
-  seg = sr.x;
-}
 
 __device__ __forceinline__ void cta_insert(unsigned pend, uint64_t key, uint32_t seg,
                                            int lane, uint32_t k, volatile uint64_t* s_thr,
@@ -144,46 +120,288 @@ __device__ __forceinline__ void cta_insert(unsigned pend, uint64_t key, uint32_t
   }
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kScoreThreads) score_topk_kernel(const __grid_constant__ ScoreParams p) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  SmemArch sa = build_arch_tables<MODE>(p.archs, smem);
-  const size_t arch_bytes = align16(arch_smem_bytes(p.archs));
-  volatile uint64_t* s_thr = reinterpret_cast<volatile uint64_t*>(smem + arch_bytes);
-  volatile uint64_t* s_list = s_thr + p.n_seg;
-  int* s_lock = reinterpret_cast<int*>(const_cast<uint64_t*>(s_list + (size_t)p.n_seg * p.k));
-  for (uint32_t i = threadIdx.x; i < p.n_seg; i += blockDim.x) {
-    s_thr[i] = 0;
-    s_lock[i] = 0;
-  }
-  for (uint32_t i = threadIdx.x; i < p.n_seg * p.k; i += blockDim.x) s_list[i] = 0;
-  __syncthreads();
+// Per-warp top-k list held in registers (lane j < k: j-th best key of the
+// warp's current segment).  Candidates are offered against the warp's own
+// exact threshold, so the common case costs one 64-bit compare and a ballot
+// and improvement bursts need no lock; the list is merged into the CTA's
+// shared table (under its lock) only when the warp moves to another segment
+// and at the end of the chunk.
+constexpr uint32_t kNoSeg = 0xffffffffu;
 
+struct WarpList {
+  uint64_t v;
+  uint64_t thr;
+  uint32_t seg;
+};
+
+__device__ __forceinline__ void wl_flush(WarpList& w, int lane, uint32_t k, volatile uint64_t* s_thr,
+                                         volatile uint64_t* s_list, int* s_lock) {
+  if (w.seg != kNoSeg) {
+    const unsigned pend = __ballot_sync(0xffffffffu, lane < (int)k && w.v > s_thr[w.seg]);
+    if (pend) cta_insert(pend, w.v, w.seg, lane, k, s_thr, s_list, s_lock);
+  }
+  w.v = 0;
+  w.thr = 0;
+  w.seg = kNoSeg;
+}
+
+__device__ __forceinline__ void wl_offer(uint64_t key, uint32_t seg, WarpList& w, int lane,
+                                         uint32_t k, volatile uint64_t* s_thr,
+                                         volatile uint64_t* s_list, int* s_lock) {
+  const bool mine = seg == w.seg;
+  unsigned pend = __ballot_sync(0xffffffffu, !mine || key > w.thr);   // key 0 carries w.seg
+  if (pend == 0) return;
+  const unsigned other = pend & __ballot_sync(0xffffffffu, !mine);
+  if (other) {
+    const uint32_t s0 = __shfl_sync(0xffffffffu, seg, __ffs(other) - 1);
+    const unsigned same0 = other & __ballot_sync(0xffffffffu, seg == s0);
+    if (same0 == other && other == pend) {
+      // the warp has moved on to segment s0: publish the old list, adopt s0
+      wl_flush(w, lane, k, s_thr, s_list, s_lock);
+      w.seg = s0;
+    } else {
+      // mixed segments in one batch (segment boundary / unordered input)
+      const bool in_other = (other >> lane) & 1u;
+      const unsigned o2 = __ballot_sync(0xffffffffu, in_other && key > s_thr[seg]);
+      if (o2) cta_insert(o2, key, seg, lane, k, s_thr, s_list, s_lock);
+      pend &= ~other;
+    }
+  }
+  while (pend) {
+    const int l = __ffs(pend) - 1;
+    pend &= pend - 1;
+    const uint64_t kk = __shfl_sync(0xffffffffu, key, l);
+    if (kk > w.thr) {
+      warp_list_insert(w.v, kk, (int)k, lane);
+      w.thr = warp_list_min(w.v, (int)k);
+    }
+  }
+}
+
+// Shared-memory carve-up common to both feeds (after an optional TMA ring).
+struct K2Shared {
+  K2Ctx c;
+  volatile uint64_t* thr;
+  volatile uint64_t* list;
+  int* lock;
+};
+
+__host__ __device__ inline size_t k2_tail_bytes(const ArchParams& a, uint32_t n_var,
+                                                uint32_t n_seg, uint32_t k, bool vt_smem) {
+  size_t b = k2_arch_bytes(a);
+  if (vt_smem) b += (size_t)n_var * a.n * sizeof(occx_vent_t);
+  return b + (size_t)n_seg * 8 + (size_t)n_seg * k * 8 + (size_t)n_seg * 4 + 16 +
+         (size_t)32 * (OCCX_MAX_K + 1) * 8;
+}
+
+template <int MODE, bool VT_SMEM>
+__device__ inline K2Shared k2_setup(const ScoreParams& p, unsigned char* base) {
+  K2Shared s;
+  K2Arch* rows = reinterpret_cast<K2Arch*>(base);
+  uint32_t* tab = reinterpret_cast<uint32_t*>(base + sizeof(K2Arch) * p.archs.n);
+  k2_build<MODE>(p.archs, rows, tab);
+  unsigned char* q = base + k2_arch_bytes(p.archs);
+  const occx_vent_t* vt = p.vtab;
+  if (VT_SMEM) {
+    occx_vent_t* v = reinterpret_cast<occx_vent_t*>(q);
+    const uint32_t rows_n = p.n_var * (uint32_t)p.archs.n;
+    const uint4* src = reinterpret_cast<const uint4*>(p.vtab);
+    uint4* dst = reinterpret_cast<uint4*>(v);
+    for (uint32_t i = threadIdx.x; i < rows_n * 2; i += blockDim.x) dst[i] = src[i];
+    vt = v;
+    q += (size_t)rows_n * sizeof(occx_vent_t);
+  }
+  s.c = K2Ctx{rows, tab, vt, (uint32_t)p.archs.n, p.n_var};
+  s.thr = reinterpret_cast<volatile uint64_t*>(q);
+  s.list = s.thr + p.n_seg;
+  s.lock = reinterpret_cast<int*>(const_cast<uint64_t*>(s.list + (size_t)p.n_seg * p.k));
+  for (uint32_t i = threadIdx.x; i < p.n_seg; i += blockDim.x) {
+    s.thr[i] = 0;
+    s.lock[i] = 0;
+  }
+  for (uint32_t i = threadIdx.x; i < p.n_seg * p.k; i += blockDim.x) s.list[i] = 0;
+  return s;
+}
+
+// End of chunk: every warp stages its list; after a barrier warp 0 merges
+// the staged lists into the shared table alone (no lock traffic), then
+// the table is written out.  `stage` holds n_warps x (k keys + segment).
+__device__ inline void k2_stage(const WarpList& wl, int lane, uint32_t k, uint64_t* stage,
+                                uint32_t slot) {
+  uint64_t* row = stage + (size_t)slot * (OCCX_MAX_K + 1);
+  if (lane < (int)k) row[lane] = wl.v;
+  if (lane == 0) row[OCCX_MAX_K] = wl.seg;
+}
+
+__device__ inline void k2_merge_staged(const uint64_t* stage, uint32_t n_slots, uint32_t k,
+                                       volatile uint64_t* s_thr, volatile uint64_t* s_list,
+                                       int* s_lock) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t w = 0; w < n_slots; ++w) {
+    const uint64_t* row = stage + (size_t)w * (OCCX_MAX_K + 1);
+    const uint32_t seg = (uint32_t)row[OCCX_MAX_K];
+    if (seg == kNoSeg) continue;
+    const uint64_t key = lane < (int)k ? row[lane] : 0ull;
+    const unsigned pend = __ballot_sync(0xffffffffu, key > s_thr[seg]);
+    if (pend) cta_insert(pend, key, seg, lane, k, s_thr, s_list, s_lock);
+  }
+}
+
+__device__ inline void k2_flush(const ScoreParams& p, const K2Shared& s) {
+  uint64_t* out = p.partials + (size_t)blockIdx.x * p.n_seg * p.k;
+  for (uint32_t i = threadIdx.x; i < p.n_seg * p.k; i += blockDim.x) out[i] = s.list[i];
+}
+
+// ---- LDG feed ---------------------------------------------------------------
+constexpr int kLdgThreads = 512;
+constexpr int kLdgUnroll = 4;
+
+template <int MODE, bool VT_SMEM>
+__global__ void __launch_bounds__(kLdgThreads) score_topk_ldg_kernel(const __grid_constant__ ScoreParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const K2Shared s = k2_setup<MODE, VT_SMEM>(p, smem);
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const uint64_t begin = (uint64_t)blockIdx.x * p.chunk;
   const uint64_t end = begin + p.chunk < p.n ? begin + p.chunk : p.n;
-  constexpr int kTile = kScoreThreads * kScoreUnroll;
+  constexpr int kTile = kLdgThreads * kLdgUnroll;
+  WarpList wl{0, 0, kNoSeg};
+  K2Cache cc;
+  cc.x = cc.z = cc.w = 0xffffffffu;
+  k2_fill<VT_SMEM>(s.c, make_uint4(0xffffffffu, 0, 0, 0xffffffffu), cc);
   for (uint64_t base = begin; base < end; base += kTile) {
-    uint4 r[kScoreUnroll];
+    uint4 r[kLdgUnroll];
 #pragma unroll
-    for (int u = 0; u < kScoreUnroll; ++u) {
-      const uint64_t i = base + (uint64_t)u * kScoreThreads + threadIdx.x;
+    for (int u = 0; u < kLdgUnroll; ++u) {
+      const uint64_t i = base + (uint64_t)u * kLdgThreads + threadIdx.x;
       r[u] = (i < end) ? ld_stream(p.cand + i) : make_uint4(0, 0, 0, 0xffffffffu);
     }
+    const uint64_t inv0 = kIdxMask - p.index_base - base - threadIdx.x;
 #pragma unroll
-    for (int u = 0; u < kScoreUnroll; ++u) {
-      const uint64_t i = base + (uint64_t)u * kScoreThreads + threadIdx.x;
-      uint64_t key;
-      uint32_t seg;
-      score_one<MODE>(sa, p, r[u], p.index_base + i, key, seg);   // OOB: arch 0xff -> key 0
-      const bool want = key > s_thr[seg];
-      const unsigned pend = __ballot_sync(0xffffffffu, want);
-      if (pend) cta_insert(pend, key, seg, lane, p.k, s_thr, s_list, s_lock);
+    for (int u = 0; u < kLdgUnroll; ++u) {
+      if (!__all_sync(0xffffffffu, k2_hit(cc, r[u]))) k2_fill<VT_SMEM>(s.c, r[u], cc);
+      const uint64_t key = k2_key<MODE>(s.c, cc, r[u], inv0 - (uint64_t)u * kLdgThreads);
+      wl_offer(key, key ? cc.seg : wl.seg, wl, lane, p.k, s.thr, s.list, s.lock);
     }
   }
+  uint64_t* stage = reinterpret_cast<uint64_t*>(const_cast<int*>(s.lock + p.n_seg)) + 1;
+  stage = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(stage) + 7) & ~uintptr_t(7));
+  k2_stage(wl, lane, p.k, stage, threadIdx.x >> 5);
   __syncthreads();
-  uint64_t* out = p.partials + (size_t)blockIdx.x * p.n_seg * p.k;
-  for (uint32_t i = threadIdx.x; i < p.n_seg * p.k; i += blockDim.x) out[i] = s_list[i];
+  if (threadIdx.x < 32) k2_merge_staged(stage, kLdgThreads / 32, p.k, s.thr, s.list, s.lock);
+  __syncthreads();
+  k2_flush(p, s);
+}
+
+// ---- TMA feed ---------------------------------------------------------------
+constexpr int kTmaConsumerWarps = 16;
+constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
+constexpr int kTmaTile = 2048;                  // records per stage (32 KB)
+constexpr int kTmaStages = 4;
+constexpr int kTmaPerThread = kTmaTile / (kTmaConsumerWarps * 32);
+constexpr size_t kTmaRingBytes = (size_t)kTmaStages * kTmaTile * 16;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+template <int MODE, bool VT_SMEM>
+__global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __grid_constant__ ScoreParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint4* ring = reinterpret_cast<uint4*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTmaRingBytes);
+  uint64_t* empty = full + kTmaStages;
+  const K2Shared s = k2_setup<MODE, VT_SMEM>(p, smem + kTmaRingBytes + 2 * kTmaStages * 8);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* stage = reinterpret_cast<uint64_t*>(const_cast<int*>(s.lock + p.n_seg)) + 1;
+  stage = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(stage) + 7) & ~uintptr_t(7));
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kTmaStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kTmaConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t begin = (uint64_t)blockIdx.x * p.chunk;
+  const uint64_t end = begin + p.chunk < p.n ? begin + p.chunk : p.n;
+  const uint32_t n_tiles = begin < end ? (uint32_t)((end - begin + kTmaTile - 1) / kTmaTile) : 0u;
+  if (warp == 0) {
+    if (lane == 0) {
+      uint64_t policy;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+      for (uint32_t t = 0; t < n_tiles; ++t) {
+        const uint32_t st = t % kTmaStages;
+        mbar_wait(&empty[st], ((t / kTmaStages) & 1u) ^ 1u);
+        const uint64_t tb = begin + (uint64_t)t * kTmaTile;
+        const uint32_t cnt = (uint32_t)min((uint64_t)kTmaTile, end - tb);
+        mbar_expect_tx(&full[st], cnt * 16u);
+        tma_load_1d(ring + (size_t)st * kTmaTile, p.cand + tb, cnt * 16u, &full[st], policy);
+      }
+    }
+  } else {
+    const uint32_t ct = threadIdx.x - 32;
+    WarpList wl{0, 0, kNoSeg};
+    K2Cache cc;
+    cc.x = cc.z = cc.w = 0xffffffffu;
+    k2_fill<VT_SMEM>(s.c, make_uint4(0xffffffffu, 0, 0, 0xffffffffu), cc);
+    for (uint32_t t = 0; t < n_tiles; ++t) {
+      const uint32_t st = t % kTmaStages;
+      const uint64_t tb = begin + (uint64_t)t * kTmaTile;
+      const uint32_t cnt = (uint32_t)min((uint64_t)kTmaTile, end - tb);
+      mbar_wait(&full[st], (t / kTmaStages) & 1u);
+      const uint4* tile = ring + (size_t)st * kTmaTile;
+      uint4 r[kTmaPerThread];
+#pragma unroll
+      for (int j = 0; j < kTmaPerThread; ++j) {
+        const uint32_t idx = (uint32_t)j * (kTmaConsumerWarps * 32) + ct;
+        r[j] = idx < cnt ? tile[idx] : make_uint4(0, 0, 0, 0xffffffffu);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);      // records are in registers
+      const uint64_t inv0 = kIdxMask - p.index_base - tb - ct;
+#pragma unroll
+      for (int j = 0; j < kTmaPerThread; ++j) {
+        if (!__all_sync(0xffffffffu, k2_hit(cc, r[j]))) k2_fill<VT_SMEM>(s.c, r[j], cc);
+        const uint64_t key =
+            k2_key<MODE>(s.c, cc, r[j], inv0 - (uint64_t)j * (kTmaConsumerWarps * 32));
+        wl_offer(key, key ? cc.seg : wl.seg, wl, lane, p.k, s.thr, s.list, s.lock);
+      }
+    }
+    k2_stage(wl, lane, p.k, stage, warp - 1);
+  }
+  __syncthreads();
+  if (warp == 1) k2_merge_staged(stage, kTmaConsumerWarps, p.k, s.thr, s.list, s.lock);
+  __syncthreads();
+  k2_flush(p, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -371,6 +589,7 @@ __global__ void build_vtab_kernel(const occx_mixsum_t* __restrict__ sum,
     rank_bits = (rank < (1u << 20)) ? ((1u << 20) - 1u - rank) : 0u;
   }
   e.rank_bits = rank_bits;
+  e.key_hi = 0x80000000u | (rank_bits << 2);   // key bits 63 and 53-34, pre-shifted
   vtab[t] = e;
 }
 
@@ -482,14 +701,16 @@ extern "C" int occx_occupancy_batch(const occx_ctx* ctx, const occx_arch_t* h_ar
   return OCCX_OK;
 }
 
-static size_t score_smem_bytes(const ArchParams& a, uint32_t n_seg, uint32_t k) {
-  return align16(arch_smem_bytes(a)) + (size_t)n_seg * 8 + (size_t)n_seg * k * 8 +
-         (size_t)n_seg * 4;
+enum { kFeedTma = 0, kFeedLdg = 1 };
+
+static int score_feed() {
+  const char* e = std::getenv("OCCX_K2_FEED");      // A/B switch for benchmarking
+  return (e && e[0] == 'l') ? kFeedLdg : kFeedTma;
 }
 
 static int score_grid(const occx_ctx* ctx) {
-  // persistent: 2 CTAs of 512 threads per SM (64 warps / SM)
-  return ctx->sm_count * 2;
+  // persistent: TMA feed one 544-thread CTA per SM; LDG feed two 512-thread CTAs
+  return score_feed() == kFeedTma ? ctx->sm_count : ctx->sm_count * 2;
 }
 
 extern "C" int occx_score_workspace_bytes(const occx_ctx* ctx, uint32_t n_seg, uint32_t k,
@@ -534,20 +755,45 @@ extern "C" int occx_score_topk(const occx_ctx* ctx, const occx_arch_t* h_archs, 
   p.k = k;
   p.partials = static_cast<uint64_t*>(d_ws);
   const int grid = score_grid(ctx);
-  constexpr uint64_t tile = (uint64_t)kScoreThreads * kScoreUnroll;
+  const int feed = score_feed();
+  const uint64_t tile = feed == kFeedTma ? (uint64_t)kTmaTile : (uint64_t)kLdgThreads * kLdgUnroll;
   const uint64_t tiles = (n + tile - 1) / tile;
   p.chunk = ((tiles + grid - 1) / grid) * tile;
   if (p.chunk == 0) p.chunk = tile;
-  const size_t smem = score_smem_bytes(p.archs, n_seg, k);
-  if (smem > (size_t)ctx->max_smem_optin) return OCCX_ERR_CAPACITY;
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (mode == OCCX_MODE_CORRECTED) {
-    if (set_smem(score_topk_kernel<0>, smem)) return OCCX_ERR_CUDA;
-    score_topk_kernel<0><<<grid, kScoreThreads, smem, s>>>(p);
-  } else {
-    if (set_smem(score_topk_kernel<1>, smem)) return OCCX_ERR_CUDA;
-    score_topk_kernel<1><<<grid, kScoreThreads, smem, s>>>(p);
+  p.vt_smem = ((uint64_t)n_var * n_arch <= (uint64_t)kVtSmemMax) ? 1u : 0u;
+  size_t smem = k2_tail_bytes(p.archs, n_var, n_seg, k, p.vt_smem != 0);
+  if (feed == kFeedTma) smem += kTmaRingBytes + 2 * kTmaStages * 8;
+  if (smem > (size_t)ctx->max_smem_optin) {
+    if (!p.vt_smem) return OCCX_ERR_CAPACITY;
+    p.vt_smem = 0;
+    smem -= (size_t)n_var * n_arch * sizeof(occx_vent_t);
+    if (smem > (size_t)ctx->max_smem_optin) return OCCX_ERR_CAPACITY;
   }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+#define OCCX_LAUNCH_K2(KERNEL, THREADS)                                              \
+  do {                                                                               \
+    if (set_smem(KERNEL, smem)) return OCCX_ERR_CUDA;                                \
+    KERNEL<<<grid, THREADS, smem, s>>>(p);                                           \
+  } while (0)
+  const bool vts = p.vt_smem != 0;
+  if (feed == kFeedTma) {
+    if (mode == OCCX_MODE_CORRECTED) {
+      if (vts) OCCX_LAUNCH_K2((score_topk_tma_kernel<0, true>), kTmaThreads);
+      else OCCX_LAUNCH_K2((score_topk_tma_kernel<0, false>), kTmaThreads);
+    } else {
+      if (vts) OCCX_LAUNCH_K2((score_topk_tma_kernel<1, true>), kTmaThreads);
+      else OCCX_LAUNCH_K2((score_topk_tma_kernel<1, false>), kTmaThreads);
+    }
+  } else {
+    if (mode == OCCX_MODE_CORRECTED) {
+      if (vts) OCCX_LAUNCH_K2((score_topk_ldg_kernel<0, true>), kLdgThreads);
+      else OCCX_LAUNCH_K2((score_topk_ldg_kernel<0, false>), kLdgThreads);
+    } else {
+      if (vts) OCCX_LAUNCH_K2((score_topk_ldg_kernel<1, true>), kLdgThreads);
+      else OCCX_LAUNCH_K2((score_topk_ldg_kernel<1, false>), kLdgThreads);
+    }
+  }
+#undef OCCX_LAUNCH_K2
   OCCX_CUDA_TRY(cudaGetLastError());
   if (d_topk == nullptr) return OCCX_OK;     // partials only: [grid][n_seg][k] in d_ws
   return occx_topk_merge(ctx, p.partials, (uint32_t)grid, n_seg, k, d_topk, stream);
