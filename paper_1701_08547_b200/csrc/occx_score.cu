@@ -252,12 +252,46 @@ __device__ inline void k2_flush(const ScoreParams& p, const K2Shared& s) {
   for (uint32_t i = threadIdx.x; i < p.n_seg * p.k; i += blockDim.x) out[i] = s.list[i];
 }
 
+// Four records of one thread (the warp's 128-record slice: j*32 + lane).
+// Common case: one VOTE.ALL (cache valid for all four) and one VOTE.ANY
+// (nothing beats the warp list) for four candidates.
+template <int MODE, bool VT_SMEM>
+__device__ __forceinline__ void k2_process4(const K2Shared& s, K2Cache& cc, WarpList& wl,
+                                            const uint4 (&r)[4], const uint64_t inv, int lane,
+                                            uint32_t k) {
+  uint64_t key[4];
+  uint32_t seg[4];
+  const bool hit = k2_hit(cc, r[0]) & k2_hit(cc, r[1]) & k2_hit(cc, r[2]) & k2_hit(cc, r[3]);
+  if (__all_sync(0xffffffffu, hit)) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      key[j] = k2_key<MODE>(s.c, cc, r[j], inv - 32u * j);
+      seg[j] = cc.seg;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (!__all_sync(0xffffffffu, k2_hit(cc, r[j]))) k2_fill<VT_SMEM>(s.c, r[j], cc);
+      key[j] = k2_key<MODE>(s.c, cc, r[j], inv - 32u * j);
+      seg[j] = cc.seg;
+    }
+  }
+  bool any = false;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) any |= key[j] != 0 && (seg[j] != wl.seg || key[j] > wl.thr);
+  if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      wl_offer(key[j], key[j] ? seg[j] : wl.seg, wl, lane, k, s.thr, s.list, s.lock);
+  }
+}
+
 // ---- LDG feed ---------------------------------------------------------------
 constexpr int kLdgThreads = 512;
 constexpr int kLdgUnroll = 4;
 
 template <int MODE, bool VT_SMEM>
-__global__ void __launch_bounds__(kLdgThreads) score_topk_ldg_kernel(const __grid_constant__ ScoreParams p) {
+__global__ void __launch_bounds__(kLdgThreads, 2) score_topk_ldg_kernel(const __grid_constant__ ScoreParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const K2Shared s = k2_setup<MODE, VT_SMEM>(p, smem);
   __syncthreads();
@@ -265,24 +299,20 @@ __global__ void __launch_bounds__(kLdgThreads) score_topk_ldg_kernel(const __gri
   const uint64_t begin = (uint64_t)blockIdx.x * p.chunk;
   const uint64_t end = begin + p.chunk < p.n ? begin + p.chunk : p.n;
   constexpr int kTile = kLdgThreads * kLdgUnroll;
+  static_assert(kLdgUnroll == 4, "k2_process4");
   WarpList wl{0, 0, kNoSeg};
   K2Cache cc;
   cc.x = cc.z = cc.w = 0xffffffffu;
   k2_fill<VT_SMEM>(s.c, make_uint4(0xffffffffu, 0, 0, 0xffffffffu), cc);
+  const uint32_t slice = (threadIdx.x >> 5) * 128u + lane;     // warp-contiguous 128 records
   for (uint64_t base = begin; base < end; base += kTile) {
-    uint4 r[kLdgUnroll];
+    uint4 r[4];
 #pragma unroll
-    for (int u = 0; u < kLdgUnroll; ++u) {
-      const uint64_t i = base + (uint64_t)u * kLdgThreads + threadIdx.x;
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t i = base + slice + 32u * u;
       r[u] = (i < end) ? ld_stream(p.cand + i) : make_uint4(0, 0, 0, 0xffffffffu);
     }
-    const uint64_t inv0 = kIdxMask - p.index_base - base - threadIdx.x;
-#pragma unroll
-    for (int u = 0; u < kLdgUnroll; ++u) {
-      if (!__all_sync(0xffffffffu, k2_hit(cc, r[u]))) k2_fill<VT_SMEM>(s.c, r[u], cc);
-      const uint64_t key = k2_key<MODE>(s.c, cc, r[u], inv0 - (uint64_t)u * kLdgThreads);
-      wl_offer(key, key ? cc.seg : wl.seg, wl, lane, p.k, s.thr, s.list, s.lock);
-    }
+    k2_process4<MODE, VT_SMEM>(s, cc, wl, r, kIdxMask - p.index_base - base - slice, lane, p.k);
   }
   uint64_t* stage = reinterpret_cast<uint64_t*>(const_cast<int*>(s.lock + p.n_seg)) + 1;
   stage = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(stage) + 7) & ~uintptr_t(7));
@@ -298,7 +328,7 @@ constexpr int kTmaConsumerWarps = 16;
 constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
 constexpr int kTmaTile = 2048;                  // records per stage (32 KB)
 constexpr int kTmaStages = 4;
-constexpr int kTmaPerThread = kTmaTile / (kTmaConsumerWarps * 32);
+static_assert(kTmaTile == kTmaConsumerWarps * 128, "4 records per consumer thread");
 constexpr size_t kTmaRingBytes = (size_t)kTmaStages * kTmaTile * 16;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -368,7 +398,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
       }
     }
   } else {
-    const uint32_t ct = threadIdx.x - 32;
     WarpList wl{0, 0, kNoSeg};
     K2Cache cc;
     cc.x = cc.z = cc.w = 0xffffffffu;
@@ -379,22 +408,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
       const uint32_t cnt = (uint32_t)min((uint64_t)kTmaTile, end - tb);
       mbar_wait(&full[st], (t / kTmaStages) & 1u);
       const uint4* tile = ring + (size_t)st * kTmaTile;
-      uint4 r[kTmaPerThread];
+      const uint32_t slice = (uint32_t)(warp - 1) * 128u + lane;
+      uint4 r[4];
 #pragma unroll
-      for (int j = 0; j < kTmaPerThread; ++j) {
-        const uint32_t idx = (uint32_t)j * (kTmaConsumerWarps * 32) + ct;
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t idx = slice + 32u * j;
         r[j] = idx < cnt ? tile[idx] : make_uint4(0, 0, 0, 0xffffffffu);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);      // records are in registers
-      const uint64_t inv0 = kIdxMask - p.index_base - tb - ct;
-#pragma unroll
-      for (int j = 0; j < kTmaPerThread; ++j) {
-        if (!__all_sync(0xffffffffu, k2_hit(cc, r[j]))) k2_fill<VT_SMEM>(s.c, r[j], cc);
-        const uint64_t key =
-            k2_key<MODE>(s.c, cc, r[j], inv0 - (uint64_t)j * (kTmaConsumerWarps * 32));
-        wl_offer(key, key ? cc.seg : wl.seg, wl, lane, p.k, s.thr, s.list, s.lock);
-      }
+      k2_process4<MODE, VT_SMEM>(s, cc, wl, r, kIdxMask - p.index_base - tb - slice, lane, p.k);
     }
     k2_stage(wl, lane, p.k, stage, warp - 1);
   }
