@@ -36,10 +36,11 @@ def allgather_merge(local_table, merge: Callable, group=None):
     world = dist.get_world_size(group)
     if world == 1:
         return local_table
-    gathered = torch.empty((world, *local_table.shape), dtype=local_table.dtype,
+    n_seg, k = local_table.shape
+    gathered = torch.empty((world * n_seg, k), dtype=local_table.dtype,
                            device=local_table.device)
     dist.all_gather_into_tensor(gathered, local_table.contiguous(), group=group)
-    return merge(gathered)
+    return merge(gathered.view(world, n_seg, k))
 
 
 def score_space_sharded(plan, group=None, chunk: int = 1 << 28, records=None,

@@ -1,0 +1,68 @@
+"""The C-ABI library loads on a CPU-only host, exports every symbol that
+include/occx.h declares, and its host-only entry points behave (no GPU
+compute is attempted here)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from paper_1701_08547_b200 import _lib, workloads
+from paper_1701_08547_b200.arch import ARCH_DTYPE, pack_archs
+
+
+@pytest.fixture(scope="module")
+def lib():
+    return _lib.load()
+
+
+def test_exports_every_header_function(lib):
+    names = _lib.header_functions()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(_lib.SIGNATURES), "binding and header disagree"
+
+
+def test_abi_version_and_status_strings(lib):
+    assert lib.occx_abi_version() == 1
+    for code in range(11):
+        assert lib.occx_status_string(code)
+    assert b"IllegalLaunchError" in lib.occx_status_string(2)
+
+
+def test_struct_sizes_match_header():
+    # sizes asserted in _lib against the C layout; re-check the arch row
+    assert ARCH_DTYPE.itemsize == 40
+    assert _lib.CAND.itemsize == 16 and _lib.OCC.itemsize == 32
+    assert _lib.VENT.itemsize == 32 and _lib.SEGDESC.itemsize == 80
+
+
+def test_check_archs_host_only(lib):
+    a = pack_archs(workloads.all_archs())
+    bad = ctypes.c_int(7)
+    assert lib.occx_check_archs(a.ctypes.data, len(a), ctypes.byref(bad)) == 0
+    assert bad.value == -1
+    b = a.copy()
+    b[2]["max_warps_per_mp"] = 200          # 7-bit key field
+    assert lib.occx_check_archs(b.ctypes.data, len(b), ctypes.byref(bad)) == 8
+    assert bad.value == 2
+    assert lib.occx_check_archs(a.ctypes.data, 0, ctypes.byref(bad)) == 8
+
+
+def test_no_gpu_fails_loudly(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    out = ctypes.c_void_p()
+    assert lib.occx_ctx_create(0, ctypes.byref(out)) == 6      # OCCX_ERR_CUDA
+    from paper_1701_08547_b200 import DeviceError, occupancy_batch
+    with pytest.raises(DeviceError):
+        occupancy_batch(workloads.all_archs()[1], [(128, 27, 0)])
+
+
+def test_null_arguments_rejected(lib):
+    assert lib.occx_occupancy_batch(None, None, 0, None, 0, 0, None, None) == 1
+    assert lib.occx_score_topk(None, None, 0, None, 0, 0, 0, None, 0, 0, 0, None, 0,
+                               None, None) == 1
+    assert lib.occx_topk_merge(None, None, 0, 0, 0, None, None) == 1
