@@ -194,7 +194,7 @@ def main():
     ap.add_argument("--mode", default="corrected", choices=["corrected", "verbatim"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=1_500_000)
+    ap.add_argument("--cpu-sample", type=int, default=4_000_000)
     ap.add_argument("--e2e-steps", type=int, default=None)
     args = ap.parse_args()
     if args.warmup < 3:
