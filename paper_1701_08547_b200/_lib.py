@@ -67,6 +67,8 @@ SIGNATURES = {
                          _P, _P], _I),
     "occx_topk_merge": ([_P, _P, _U32, _U32, _U32, _P, _P], _I),
     "occx_gen_space": ([_P, _P, _U32, _P, _U64, _U64, _P, _P], _I),
+    "occx_score_space": ([_P, _P, _I, _P, _U32, _P, _U32, _U64, _U64, _I, _P, _U32, _U32, _U32,
+                          _P, _U64, _P, _P], _I),
 }
 
 

@@ -219,8 +219,8 @@ class SignatureTable:
         sid = self.ids.get(key)
         if sid is None:
             sid = len(self.classes)
-            if sid >= 65536:
-                raise DeviceError("more than 65536 distinct instruction signatures")
+            if sid >= 65535:
+                raise DeviceError("more than 65535 distinct instruction signatures")
             self.ids[key] = sid
             self.classes.append(DEVICE_ID[classify_signature(opcode, key[1], self.table)])
         return sid
@@ -502,6 +502,7 @@ class ScorePlan:
         self.mixes = mixes
         torch = _torch()
         self.d_desc = _to_device(desc)
+        self.n_pool = max(len(pool), 1)
         self.d_pool = _to_device(np.asarray(pool or [0], np.uint32))
         # K1 on device, then the feature table
         cols = [int(a["cost_key"]) for a in self.h_archs]
@@ -594,6 +595,23 @@ class ScorePlan:
             return tables[0]
         return self.merge(tables, n_chunks)
 
+    def score_implicit(self, begin: int = 0, n: int | None = None, out=None, stream=None,
+                       merge: bool = True):
+        """K2i: score candidates [begin, begin+n) of the space decoded from their
+        global index inside the kernel (no records in HBM).  Identical keys to
+        generate() + score(); returns the device [n_seg, k] table."""
+        torch = _torch()
+        n = self.total - begin if n is None else n
+        if merge and out is None:
+            out = torch.empty((self.n_seg, self.k), dtype=torch.int64, device="cuda")
+        _lib.check(_lib.load().occx_score_space(
+            _lib.ctx(), _lib.ptr(self.h_archs), self.n_arch, _lib.ptr(self.d_desc), self.n_seg,
+            _lib.ptr(self.d_pool), self.n_pool, begin, n, MODE_CODE[self.mode],
+            _lib.ptr(self.d_vtab), self.n_var, self.n_seg, self.k, _lib.ptr(self.d_ws),
+            self.ws_bytes, _lib.ptr(out) if merge else None, _lib.stream_ptr(stream)),
+            "occx_score_space")
+        return out if merge else self.d_ws
+
     def merge(self, d_lists, n_lists: int, out=None, stream=None):
         """K3 over [n_lists, n_seg, k] device tables -> [n_seg, k]."""
         torch = _torch()
@@ -659,22 +677,10 @@ class ctypes_u64:
 
 
 def score_space(kernels: Sequence[KernelSpec], archs: Sequence[ArchSpec],
-                mode: Mode = Mode.CORRECTED, k: int = 16,
-                chunk: int = 1 << 27) -> list[SegmentTopK]:
+                mode: Mode = Mode.CORRECTED, k: int = 16) -> list[SegmentTopK]:
     """Score every candidate of the kernels' spaces on every arch; return
-    the top-k configurations per (kernel, arch).  Candidates are decoded on
-    the device chunk by chunk (chunk x 16 B of HBM) and scored by K2; the
-    per-chunk tables are merged by K3."""
-    torch = _torch()
+    the top-k configurations per (kernel, arch).  Candidates are decoded
+    from their index inside the scorer (K2i): nothing but the space
+    description, the feature table and the top-k table touch HBM."""
     plan = ScorePlan(kernels, archs, mode, k)
-    tables = []
-    buf = _empty(min(chunk, plan.total) * 16)
-    for begin in range(0, plan.total, chunk):
-        n = min(chunk, plan.total - begin)
-        plan.generate(begin, n, out=buf)
-        tables.append(plan.score(buf, n, index_base=begin))
-    if len(tables) == 1:
-        keys = tables[0]
-    else:
-        keys = plan.merge(torch.stack(tables), len(tables))
-    return plan.decode(keys)
+    return plan.decode(plan.score_implicit())

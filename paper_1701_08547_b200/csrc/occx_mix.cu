@@ -7,14 +7,18 @@
 //   if guard and cls not CTRL:     mix.py:258-259 (Unclassified included:
 //       counts[PredIns] += 1        CATEGORY_OF.get(UNCLASSIFIED) is None)
 //   reg_operands += regops         mix.py:260
-// Counting uses sixteen 8-bit lane-private counters packed in four u32
-// registers (flushed with __reduce_add_sync before they can overflow), so
-// the per-record work is shifts and adds -- no shared-memory atomics.
+//
+// Counting: each lane keeps sixteen 8-bit counters packed in four u32
+// registers.  A second 32-entry table indexed by (class | guard << 4) holds
+// the 16-byte increment vector of each case (the class byte, plus the
+// PredIns byte when the guard counts), so a record costs one LDS.U8, one
+// LDS.128 and four IADDs.  Counters are reduced with 16-bit-lane REDUX.SUM
+// (bytes 0/2 and 1/3 separately) before they can overflow.
 // Dict insertion order (it decides the summation order of the FLOPS terms
 // in mix.py:278) is recovered as first_key[c] = min over occurrences of
-// 2*i (class of instruction i) or 2*i+1 (guard PredIns of instruction i):
-// a warp OR-reduction per chunk detects classes not seen before and only
-// then computes their first position.
+// 2*i (class of instruction i) or 2*i+1 (guard PredIns of instruction i);
+// a warp OR-reduction per chunk finds classes not seen before and only
+// then are their first positions located (ballots, warp-uniform).
 #include "occx_common.cuh"
 
 using namespace occx;
@@ -22,16 +26,11 @@ using namespace occx;
 namespace {
 
 constexpr int kMixThreads = 256;
-constexpr int kMixUnroll = 4;                         // records per lane per chunk
-constexpr int kFlushChunks = 255 / (2 * kMixUnroll);  // byte counters cannot overflow
+constexpr int kMixPer = 8;                            // records per lane per chunk
+constexpr int kFlushChunks = 255 / (2 * kMixPer);     // byte counters cannot overflow
 constexpr uint32_t kPred = 11;                        // OpClass.PREDICATE device id
 constexpr uint32_t kAbsent = 0xffffffffu;
-
-__device__ __forceinline__ uint32_t shl_clamp(uint32_t v, uint32_t s) {
-  uint32_t r;
-  asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(v), "r"(s));   // s >= 32 -> 0
-  return r;
-}
+constexpr uint32_t kNullClass = 15;                   // padding record: counts nothing
 
 struct MixParams {
   const uint32_t* instr;
@@ -39,101 +38,134 @@ struct MixParams {
   uint32_t n_kernels;
   const uint8_t* sig_class;
   uint32_t n_sig;
-  uint32_t lut_in_smem;
   occx_mix_t* out;
 };
 
-__global__ void __launch_bounds__(kMixThreads) mix_reduce_kernel(const __grid_constant__ MixParams p) {
-  extern __shared__ __align__(16) unsigned char s_lut[];
-  // LUT entry: bits 0-3 class id, bit 4 = "a guard adds PredIns" (class not CTRL)
-  const uint8_t* lut = p.sig_class;
-  if (p.lut_in_smem) {
-    for (uint32_t i = threadIdx.x; i < p.n_sig; i += blockDim.x) {
-      const uint32_t c = p.sig_class[i] & 15u;
-      s_lut[i] = (uint8_t)(c | ((c >= 11 && c <= 13) ? 0u : 16u));
-    }
-    __syncthreads();
-    lut = s_lut;
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
+  return v;
+}
+
+// Sum the 16 packed byte counters over the warp; lane c < 16 receives
+// class c's total.  Bytes 0/2 and 1/3 are reduced in separate 16-bit lanes
+// (32 x 255 < 2^16), 8 REDUX.SUM for 16 counters.
+__device__ __forceinline__ void reduce_counters(const uint32_t (&w)[4], int lane,
+                                                uint32_t& total) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t even = __reduce_add_sync(0xffffffffu, w[q] & 0x00ff00ffu);
+    const uint32_t odd = __reduce_add_sync(0xffffffffu, (w[q] >> 8) & 0x00ff00ffu);
+    const int c = 4 * q;
+    if (lane == c) total += even & 0xffffu;
+    if (lane == c + 1) total += odd & 0xffffu;
+    if (lane == c + 2) total += even >> 16;
+    if (lane == c + 3) total += odd >> 16;
   }
+}
+
+__global__ void __launch_bounds__(kMixThreads) mix_reduce_kernel(const __grid_constant__ MixParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint4* inc = reinterpret_cast<uint4*>(smem);              // [32] increment vectors
+  unsigned char* lut = smem + 32 * sizeof(uint4);           // [n_sig + 1] class ids
+  for (uint32_t i = threadIdx.x; i < 32; i += blockDim.x) {
+    const uint32_t c = i & 15u, g = i >> 4;
+    uint32_t v[4] = {0, 0, 0, 0};
+    if (c < 15) {
+      v[c >> 2] += 1u << ((c & 3) * 8);
+      if (g && !(c >= 11 && c <= 13)) {
+        v[kPred >> 2] += 1u << ((kPred & 3) * 8);
+        v[3] += 1u << 24;               // byte 15: "guard added a PredIns" marker
+      }
+    }
+    inc[i] = make_uint4(v[0], v[1], v[2], v[3]);
+  }
+  for (uint32_t i = threadIdx.x; i <= p.n_sig; i += blockDim.x)
+    lut[i] = i < p.n_sig ? (uint8_t)(p.sig_class[i] & 15u) : (uint8_t)kNullClass;
+  __syncthreads();
+  const uint32_t inc_base = (uint32_t)__cvta_generic_to_shared(inc);
+  const uint32_t lut_base = (uint32_t)__cvta_generic_to_shared(lut);
+  const uint32_t null_rec = p.n_sig;                        // sig = n_sig -> class 15
+
   const int lane = threadIdx.x & 31;
   const uint32_t warps_total = gridDim.x * (kMixThreads / 32);
   for (uint32_t kern = blockIdx.x * (kMixThreads / 32) + (threadIdx.x >> 5); kern < p.n_kernels;
        kern += warps_total) {
     const uint64_t beg = p.off[kern], end = p.off[kern + 1];
-    uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;   // 16 byte counters
-    uint32_t total = 0;                         // lane c < 16 holds counts[c]
-    uint32_t first = kAbsent;                   // lane c holds first_key[c]; lane 16 guard-pred
+    uint32_t w[4] = {0, 0, 0, 0};     // 16 byte counters
+    uint32_t total = 0;               // lane c < 16 holds counts[c]
+    uint32_t first = kAbsent;         // lane c holds first_key[c]; lane 16 guard-PredIns
     uint32_t regs = 0;
     uint32_t warp_seen = 0;
     int since_flush = 0;
-    for (uint64_t base = beg; base < end; base += 32 * kMixUnroll) {
-      uint32_t rec[kMixUnroll];
+    uint32_t rec[kMixPer];
 #pragma unroll
-      for (int u = 0; u < kMixUnroll; ++u) {
-        const uint64_t i = base + (uint64_t)u * 32 + lane;
-        rec[u] = (i < end) ? __ldcs(p.instr + i) : 0xffffffffu;
+    for (int u = 0; u < kMixPer; ++u) {
+      const uint64_t i = beg + (uint64_t)u * 32 + lane;
+      rec[u] = (i < end) ? __ldcs(p.instr + i) : null_rec;
+    }
+    for (uint64_t base = beg; base < end; base += 32 * kMixPer) {
+      // prefetch the next chunk while this one is processed
+      uint32_t nxt[kMixPer];
+      const uint64_t nb = base + 32 * kMixPer;
+#pragma unroll
+      for (int u = 0; u < kMixPer; ++u) {
+        const uint64_t i = nb + (uint64_t)u * 32 + lane;
+        nxt[u] = (i < end) ? __ldcs(p.instr + i) : null_rec;
       }
-      uint32_t seen = 0;
-      uint32_t cls[kMixUnroll], gp[kMixUnroll];
+      uint32_t bits[kMixPer], seen = 0;
 #pragma unroll
-      for (int u = 0; u < kMixUnroll; ++u) {
+      for (int u = 0; u < kMixPer; ++u) {
         const uint32_t r = rec[u];
-        const bool valid = r != 0xffffffffu;
-        uint32_t sig = r & 0xffffu;
-        uint32_t e;
-        if (p.lut_in_smem) e = lut[sig < p.n_sig ? sig : 0];
-        else {
-          const uint32_t c = __ldg(lut + (sig < p.n_sig ? sig : 0)) & 15u;
-          e = c | ((c >= 11 && c <= 13) ? 0u : 16u);
-        }
-        const uint32_t c = valid ? (e & 15u) : 15u;          // 15 = nothing
-        const uint32_t g = valid ? ((r >> 24) & (e >> 4) & 1u) : 0u;
-        const uint32_t sh = valid ? c * 8u : 128u;
-        w0 += shl_clamp(1u, sh);
-        w1 += shl_clamp(1u, sh - 32u);
-        w2 += shl_clamp(1u, sh - 64u) + (g << 24);          // PredIns byte 11
-        w3 += shl_clamp(1u, sh - 96u);
-        regs += valid ? ((r >> 16) & 0xffu) : 0u;
-        seen |= (valid ? (1u << c) : 0u) | (g << 16);
-        cls[u] = c;
-        gp[u] = g;
+        const uint32_t c = lds_u8(lut_base + (r & 0xffffu));
+        const uint32_t idx = c | ((r >> 20) & 16u);          // guard bit 24 -> bit 4
+        const uint4 d = lds_v4(inc_base + idx * 16u);
+        w[0] += d.x;
+        w[1] += d.y;
+        w[2] += d.z;
+        w[3] += d.w;
+        regs += __byte_perm(r, 0, 0x4442);                  // register operands (byte 2)
+        // class bit (bit 15 = padding, masked below) + guard-PredIns at bit 16
+        bits[u] = (1u << c) | ((d.w >> 24) << 16);
+        seen |= bits[u];
       }
-      const uint32_t chunk_seen = __reduce_or_sync(0xffffffffu, seen);
+      const uint32_t chunk_seen = __reduce_or_sync(0xffffffffu, seen) & 0x17fffu;
       uint32_t fresh = chunk_seen & ~warp_seen;
       if (fresh) {
         warp_seen |= chunk_seen;
-        while (fresh) {
-          const uint32_t b = __ffs(fresh) - 1;
-          fresh &= fresh - 1;
-          uint32_t best = kAbsent;
+        // walk the slots in order: a class first seen in slot u gets one
+        // ballot over that slot (all warp-uniform except the ballot)
+        uint32_t left = fresh;
 #pragma unroll
-          for (int u = 0; u < kMixUnroll; ++u) {
-            const uint32_t pos = (uint32_t)(base - beg) + (uint32_t)u * 32 + lane;
-            const bool hit = (b == 16) ? (gp[u] != 0) : (cls[u] == b);
-            const uint32_t key = 2u * pos + (b == 16 ? 1u : 0u);
-            if (hit && key < best) best = key;
+        for (int u = 0; u < kMixPer; ++u) {
+          uint32_t f = left & __reduce_or_sync(0xffffffffu, bits[u]);
+          left &= ~f;
+          while (f) {
+            const uint32_t b = __ffs(f) - 1;
+            f &= f - 1;
+            const unsigned m = __ballot_sync(0xffffffffu, (bits[u] >> b) & 1u);
+            const uint32_t pos = (uint32_t)(base - beg) + (uint32_t)u * 32 + (__ffs(m) - 1);
+            if (lane == (int)b) first = 2u * pos + (b == 16 ? 1u : 0u);
           }
-          best = __reduce_min_sync(0xffffffffu, best);
-          if (lane == (int)b) first = best;
+          if (left == 0) break;
         }
       }
       if (++since_flush == kFlushChunks) {
         since_flush = 0;
-#pragma unroll
-        for (int c = 0; c < 15; ++c) {
-          const uint32_t word = c < 4 ? w0 : c < 8 ? w1 : c < 12 ? w2 : w3;
-          const uint32_t v = __reduce_add_sync(0xffffffffu, (word >> ((c & 3) * 8)) & 0xffu);
-          if (lane == c) total += v;
-        }
-        w0 = w1 = w2 = w3 = 0;
+        reduce_counters(w, lane, total);
+        w[0] = w[1] = w[2] = w[3] = 0;
       }
-    }
 #pragma unroll
-    for (int c = 0; c < 15; ++c) {
-      const uint32_t word = c < 4 ? w0 : c < 8 ? w1 : c < 12 ? w2 : w3;
-      const uint32_t v = __reduce_add_sync(0xffffffffu, (word >> ((c & 3) * 8)) & 0xffu);
-      if (lane == c) total += v;
+      for (int u = 0; u < kMixPer; ++u) rec[u] = nxt[u];
     }
+    reduce_counters(w, lane, total);
     const uint32_t gfirst = __shfl_sync(0xffffffffu, first, 16);
     if (lane == (int)kPred && gfirst < first) first = gfirst;
     const uint32_t reg_total = __reduce_add_sync(0xffffffffu, regs);
@@ -156,7 +188,7 @@ extern "C" int occx_mix_reduce(const occx_ctx* ctx, const uint32_t* d_instr,
                                const uint64_t* d_kernel_off, uint32_t n_kernels,
                                const uint8_t* d_sig_class, uint32_t n_sig, occx_mix_t* d_out,
                                void* stream) {
-  if (!ctx || n_sig == 0 || n_sig > 65536) return OCCX_ERR_VALUE;
+  if (!ctx || n_sig == 0 || n_sig > 65535) return OCCX_ERR_VALUE;
   if (n_kernels == 0) return OCCX_OK;
   MixParams p{};
   p.instr = d_instr;
@@ -164,12 +196,19 @@ extern "C" int occx_mix_reduce(const occx_ctx* ctx, const uint32_t* d_instr,
   p.n_kernels = n_kernels;
   p.sig_class = d_sig_class;
   p.n_sig = n_sig;
-  p.lut_in_smem = n_sig <= 48 * 1024 ? 1u : 0u;
   p.out = d_out;
-  const size_t smem = p.lut_in_smem ? n_sig : 0;
-  const uint32_t warps = n_kernels;
-  const uint32_t want = (warps + kMixThreads / 32 - 1) / (kMixThreads / 32);
-  const uint32_t cap = (uint32_t)ctx->sm_count * 8;
+  const size_t smem = 32 * 16 + ((n_sig + 1 + 15) & ~15u);
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(mix_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem) != cudaSuccess)
+    return OCCX_ERR_CUDA;
+  // persistent: exactly one wave (LUT staged once per CTA, no tail wave)
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mix_reduce_kernel, kMixThreads,
+                                                    smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  const uint32_t want = (n_kernels + kMixThreads / 32 - 1) / (kMixThreads / 32);
+  const uint32_t cap = (uint32_t)ctx->sm_count * (uint32_t)per_sm;
   const uint32_t grid = want < cap ? want : cap;
   mix_reduce_kernel<<<grid, kMixThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(p);
   OCCX_CUDA_TRY(cudaGetLastError());

@@ -323,6 +323,149 @@ __global__ void __launch_bounds__(kLdgThreads, 2) score_topk_ldg_kernel(const __
   k2_flush(p, s);
 }
 
+// ---- implicit-grid feed (no records) ---------------------------------------
+// Candidates are decoded from their global index (enumerate_space order,
+// tuning.py:75-77) instead of being read: only the (R, S) digits change
+// between neighbouring candidates, so each thread caches its current
+// (TC, BC, UIF, PL, CFLAGS) block and derives R/S with one invariant-divisor
+// multiply (Granlund-Montgomery) and two table loads.  The synthesized
+// record is bit-identical to what gen_space_kernel writes, so keys match the
+// record path exactly.
+struct FastDiv {
+  uint32_t m, s1, s2;
+};
+
+__device__ __forceinline__ FastDiv fastdiv_make(uint32_t d) {
+  if (d <= 1) return FastDiv{1u, 0u, 0u};
+  const uint32_t l = 32 - __clz(d - 1);                               // ceil(log2 d)
+  const uint64_t m = ((1ull << 32) * ((1ull << l) - d)) / d + 1;     // < 2^32
+  return FastDiv{(uint32_t)m, 1u, l - 1};
+}
+__device__ __forceinline__ uint32_t fastdiv(uint32_t x, const FastDiv& f) {
+  const uint32_t t = __umulhi(x, f.m);
+  return (t + ((x - t) >> f.s1)) >> f.s2;
+}
+
+struct IgCache {
+  uint64_t blk_lo;       // global index of the current block's first candidate
+  uint32_t blk_n;        // candidates per block = |REGS| * |SMEM|
+  uint32_t n_s, r_off, s_off;
+  FastDiv ds;
+  uint32_t x, z, w_hi;   // record words: variant, T | BC << 16, arch << 16 | PL << 24
+};
+
+struct SpaceParams {
+  ScoreParams sp;        // archs, vtab, n_var, n_seg, k, chunk, partials (cand unused)
+  const occx_segdesc_t* desc;
+  const uint32_t* pool;
+  uint32_t n_desc, n_pool, pool_smem, pad;
+  uint64_t begin;        // global index of the first candidate scored
+};
+
+__device__ __noinline__ void ig_fill(const SpaceParams& q, const uint32_t* pool, uint64_t g,
+                                     IgCache& c) {
+  uint32_t lo = 0, hi = q.n_desc;                      // last segment with start <= g
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(&q.desc[mid].start) <= g) lo = mid; else hi = mid;
+  }
+  const occx_segdesc_t* d = q.desc + lo;
+  const uint64_t start = __ldg(&d->start);
+  uint32_t off[7], len[7];
+#pragma unroll
+  for (int i = 0; i < 7; ++i) {
+    off[i] = __ldg(&d->dim_off[i]);
+    len[i] = __ldg(&d->dim_len[i]);
+  }
+  const uint64_t blk = (uint64_t)len[5] * len[6];
+  uint64_t o = (g - start) / blk;
+  c.blk_lo = start + o * blk;
+  c.blk_n = (uint32_t)blk;
+  const uint32_t i_cf = (uint32_t)(o % len[4]);
+  o /= len[4];
+  const uint32_t i_pl = (uint32_t)(o % len[3]);
+  o /= len[3];
+  const uint32_t i_uif = (uint32_t)(o % len[2]);
+  o /= len[2];
+  const uint32_t i_bc = (uint32_t)(o % len[1]);
+  const uint32_t i_tc = (uint32_t)(o / len[1]);
+  const uint32_t T = pool[off[0] + i_tc], B = pool[off[1] + i_bc];
+  c.x = __ldg(&d->var_base) + i_uif * len[4] + i_cf;
+  c.z = min(T, 0xffffu) | (min(B, 0xffffu) << 16);
+  c.w_hi = ((__ldg(&d->arch) & 0xffu) << 16) | ((i_pl & 0xffu) << 24);
+  c.n_s = len[6];
+  c.r_off = off[5];
+  c.s_off = off[6];
+  c.ds = fastdiv_make(len[6]);
+}
+
+__device__ __forceinline__ uint4 ig_record(const IgCache& c, const uint32_t* pool, uint64_t g) {
+  const uint32_t rs = (uint32_t)(g - c.blk_lo);
+  const uint32_t ri = fastdiv(rs, c.ds);
+  const uint32_t si = rs - ri * c.n_s;
+  const uint32_t R = pool[c.r_off + ri], S = pool[c.s_off + si];
+  return make_uint4(c.x, S, c.z, min(R, 0xffffu) | c.w_hi);
+}
+
+template <int MODE, bool VT_SMEM>
+__global__ void __launch_bounds__(kLdgThreads, 2) score_space_kernel(const __grid_constant__ SpaceParams q) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const ScoreParams& p = q.sp;
+  const K2Shared s = k2_setup<MODE, VT_SMEM>(p, smem);
+  uint64_t* stage = reinterpret_cast<uint64_t*>(const_cast<int*>(s.lock + p.n_seg)) + 1;
+  stage = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(stage) + 7) & ~uintptr_t(7));
+  const uint32_t* pool = q.pool;
+  if (q.pool_smem) {
+    uint32_t* sp = reinterpret_cast<uint32_t*>(stage + 32 * (OCCX_MAX_K + 1));
+    for (uint32_t i = threadIdx.x; i < q.n_pool; i += blockDim.x) sp[i] = __ldg(q.pool + i);
+    pool = sp;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint64_t begin = q.begin + (uint64_t)blockIdx.x * p.chunk;
+  const uint64_t stop = q.begin + p.n;
+  const uint64_t end = begin + p.chunk < stop ? begin + p.chunk : stop;
+  constexpr int kTile = kLdgThreads * 4;
+  WarpList wl{0, 0, kNoSeg};
+  K2Cache cc;
+  cc.x = cc.z = cc.w = 0xffffffffu;
+  k2_fill<VT_SMEM>(s.c, make_uint4(0xffffffffu, 0, 0, 0xffffffffu), cc);
+  IgCache ic;
+  ic.blk_lo = 0;
+  ic.blk_n = 0;
+  const uint32_t slice = (threadIdx.x >> 5) * 128u + lane;
+  for (uint64_t base = begin; base < end; base += kTile) {
+    const uint64_t g0 = base + slice;
+    bool hit = true;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t g = g0 + 32u * j;
+      hit &= (g >= end) || (g - ic.blk_lo < (uint64_t)ic.blk_n);
+    }
+    uint4 r[4];
+    if (__all_sync(0xffffffffu, hit)) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t g = g0 + 32u * j;
+        r[j] = g < end ? ig_record(ic, pool, g) : make_uint4(0, 0, 0, 0xffffffffu);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t g = g0 + 32u * j;
+        if (g < end && !(g - ic.blk_lo < (uint64_t)ic.blk_n)) ig_fill(q, pool, g, ic);
+        r[j] = g < end ? ig_record(ic, pool, g) : make_uint4(0, 0, 0, 0xffffffffu);
+      }
+    }
+    k2_process4<MODE, VT_SMEM>(s, cc, wl, r, kIdxMask - g0, lane, p.k);
+  }
+  k2_stage(wl, lane, p.k, stage, threadIdx.x >> 5);
+  __syncthreads();
+  if (threadIdx.x < 32) k2_merge_staged(stage, kLdgThreads / 32, p.k, s.thr, s.list, s.lock);
+  __syncthreads();
+  k2_flush(p, s);
+}
+
 // ---- TMA feed ---------------------------------------------------------------
 constexpr int kTmaConsumerWarps = 16;
 constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
@@ -866,4 +1009,64 @@ extern "C" int occx_gen_space(const occx_ctx* ctx, const occx_segdesc_t* d_desc,
       d_desc, n_desc, d_pool, begin, n, reinterpret_cast<uint4*>(d_out));
   OCCX_CUDA_TRY(cudaGetLastError());
   return OCCX_OK;
+}
+
+extern "C" int occx_score_space(const occx_ctx* ctx, const occx_arch_t* h_archs, int n_arch,
+                                const occx_segdesc_t* d_desc, uint32_t n_desc,
+                                const uint32_t* d_pool, uint32_t n_pool, uint64_t begin,
+                                uint64_t n, int mode, const occx_vent_t* d_vtab, uint32_t n_var,
+                                uint32_t n_seg, uint32_t k, void* d_ws, uint64_t ws_bytes,
+                                uint64_t* d_topk, void* stream) {
+  if (!ctx || (mode != 0 && mode != 1) || k == 0 || k > OCCX_MAX_K || n_seg == 0 ||
+      n_desc == 0 || d_desc == nullptr || d_pool == nullptr)
+    return OCCX_ERR_VALUE;
+  int bad;
+  int st = occx_check_archs(h_archs, n_arch, &bad);
+  if (st) return st;
+  if (begin + n > kIdxMask + 1 || begin + n < begin) return OCCX_ERR_CAPACITY;
+  uint64_t need = 0;
+  occx_score_workspace_bytes(ctx, n_seg, k, &need);
+  if (d_ws == nullptr || ws_bytes < need) return OCCX_ERR_VALUE;
+  SpaceParams q{};
+  pack_archs(h_archs, n_arch, q.sp.archs);
+  q.sp.n = n;
+  q.sp.index_base = begin;
+  q.sp.vtab = d_vtab;
+  q.sp.n_var = n_var;
+  q.sp.n_seg = n_seg;
+  q.sp.k = k;
+  q.sp.partials = static_cast<uint64_t*>(d_ws);
+  q.desc = d_desc;
+  q.pool = d_pool;
+  q.n_desc = n_desc;
+  q.n_pool = n_pool;
+  q.begin = begin;
+  const int grid = score_grid(ctx);
+  const uint64_t tile = (uint64_t)kLdgThreads * 4;
+  const uint64_t tiles = (n + tile - 1) / tile;
+  q.sp.chunk = ((tiles + grid - 1) / grid) * tile;
+  if (q.sp.chunk == 0) q.sp.chunk = tile;
+  q.sp.vt_smem = ((uint64_t)n_var * n_arch <= (uint64_t)kVtSmemMax) ? 1u : 0u;
+  size_t smem = k2_tail_bytes(q.sp.archs, n_var, n_seg, k, q.sp.vt_smem != 0);
+  q.pool_smem = (n_pool <= 8192u) ? 1u : 0u;
+  if (q.pool_smem) smem += (size_t)n_pool * 4;
+  if (smem > (size_t)ctx->max_smem_optin) return OCCX_ERR_CAPACITY;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+#define OCCX_LAUNCH_IG(KERNEL)                                                       \
+  do {                                                                               \
+    if (set_smem(KERNEL, smem)) return OCCX_ERR_CUDA;                                \
+    KERNEL<<<grid, kLdgThreads, smem, s>>>(q);                                       \
+  } while (0)
+  const bool vts = q.sp.vt_smem != 0;
+  if (mode == OCCX_MODE_CORRECTED) {
+    if (vts) OCCX_LAUNCH_IG((score_space_kernel<0, true>));
+    else OCCX_LAUNCH_IG((score_space_kernel<0, false>));
+  } else {
+    if (vts) OCCX_LAUNCH_IG((score_space_kernel<1, true>));
+    else OCCX_LAUNCH_IG((score_space_kernel<1, false>));
+  }
+#undef OCCX_LAUNCH_IG
+  OCCX_CUDA_TRY(cudaGetLastError());
+  if (d_topk == nullptr) return OCCX_OK;
+  return occx_topk_merge(ctx, q.sp.partials, (uint32_t)grid, n_seg, k, d_topk, stream);
 }

@@ -43,14 +43,12 @@ def allgather_merge(local_table, merge: Callable, group=None):
     return merge(gathered.view(world, n_seg, k))
 
 
-def score_space_sharded(plan, group=None, chunk: int = 1 << 28, records=None,
-                        stream=None):
+def score_space_sharded(plan, group=None, records=None, stream=None):
     """Score the plan's whole space across the ranks of ``group``; every
     rank returns the merged [n_seg, k] device table.
 
     ``records``: optional pre-generated device records of this rank's shard
-    (the benchmark generates them once, untimed); otherwise the shard is
-    decoded on the device chunk by chunk.
+    (read by K2); otherwise the shard is decoded inside the scorer (K2i).
     """
     import torch
     import torch.distributed as dist
@@ -61,20 +59,7 @@ def score_space_sharded(plan, group=None, chunk: int = 1 << 28, records=None,
     if records is not None:
         local = plan.score(records, n, index_base=begin, stream=stream)
     else:
-        tables = []
-        buf = None
-        for b in range(begin, end, chunk):
-            m = min(chunk, end - b)
-            if buf is None:
-                buf = torch.empty(m * 16, dtype=torch.uint8, device="cuda")
-            plan.generate(b, m, out=buf)
-            tables.append(plan.score(buf, m, index_base=b, stream=stream))
-        if not tables:
-            local = torch.zeros((plan.n_seg, plan.k), dtype=torch.int64, device="cuda")
-        elif len(tables) == 1:
-            local = tables[0]
-        else:
-            local = plan.merge(torch.stack(tables), len(tables), stream=stream)
+        local = plan.score_implicit(begin, n, stream=stream)
     if world == 1:
         return local
     return allgather_merge(local, lambda g: plan.merge(g, g.shape[0], stream=stream), group)

@@ -299,7 +299,7 @@ def topk_golden(name):
     t0 = time.time()
     res = {"meta": META, "config": cfg.name, "total": cfg.total,
            "corrected": topk_config(cfg, R.Mode.CORRECTED)}
-    if name in ("config1", "config2"):
+    if name in ("config1", "config2", "config4"):
         res["verbatim"] = topk_config(cfg, R.Mode.VERBATIM)
     res["seconds"] = time.time() - t0
     with open(os.path.join(HERE, f"topk_{name}.json"), "w") as fh:

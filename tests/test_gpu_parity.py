@@ -323,3 +323,54 @@ def test_k2_many_segments(P, torch):
     want = oracle.score_spaces(problem_of(cfg), spaces_of(cfg), threads=8)
     assert plan.n_seg == 300
     assert np.array_equal(keys, want)
+
+
+# ---------------------------------------------------------------------------
+# K2i: implicit-grid scoring (no records)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["config1", "config2", "config4", "config5"])
+def test_k2i_implicit_golden(P, torch, golden, name):
+    import os
+    from paper_1701_08547_b200 import workloads
+    if not os.path.exists(os.path.join(os.path.dirname(__file__), "golden", f"topk_{name}.json")):
+        pytest.skip("golden missing")
+    g = golden(f"topk_{name}.json")
+    cfg = workloads.CONFIGS[name]()
+    for mode in ("corrected", "verbatim"):
+        if mode in g:
+            plan = P.ScorePlan(cfg.kernels, cfg.archs, mode, k=cfg.k)
+            keys = plan.score_implicit().cpu().numpy().view(np.uint64)
+            assert keys.tolist() == g[mode], (name, mode)
+
+
+def test_k2i_ranges_match_record_path(P, torch):
+    """Arbitrary [begin, begin+n) windows: implicit == generate + score."""
+    from paper_1701_08547_b200 import workloads
+    cfg = workloads.config4()
+    plan = P.ScorePlan(cfg.kernels, cfg.archs, k=16)
+    for begin, n in ((0, 1), (12345, 999_999), (5_242_879, 2), (plan.total - 77, 77),
+                     (31_000_003, 17_000_011)):
+        a = plan.score_implicit(begin, n).cpu().numpy()
+        b = plan.score(plan.generate(begin, n), n, index_base=begin).cpu().numpy()
+        assert np.array_equal(a, b), (begin, n)
+
+
+def test_k2i_many_segments_and_score_space(P, torch):
+    from paper_1701_08547_b200 import workloads
+    from paper_1701_08547_b200.tuning import TuningSpace
+    ks = []
+    for i in range(60):
+        space = TuningSpace(tuple(range(32, 1025, 32)), (24, 48), (1, 2), (16,),
+                            ("", "-use_fast_math"),
+                            extra=(("REGS", tuple(range(i % 7, 256, 17))),
+                                   ("SMEM", (0, 4096 * (i % 5)))))
+        ks.append(workloads.kernel_spec(workloads.KERNEL_NAMES[i % 4], space))
+    cfg = workloads.Config("many", tuple(ks), tuple(workloads.all_archs()), 8)
+    plan = P.ScorePlan(cfg.kernels, cfg.archs, k=8)
+    keys = plan.score_implicit().cpu().numpy().view(np.uint64)
+    want = oracle.score_spaces(problem_of(cfg), spaces_of(cfg), threads=8)
+    assert np.array_equal(keys, want)
+    # the public API on the same space
+    res = P.score_space(cfg.kernels[:3], cfg.archs, k=8)
+    assert [e.key for e in res[0].entries] == [int(x) for x in want[0] if x]
