@@ -181,6 +181,73 @@ def cpu_oracle_c(workload: str, mode: str, seconds_hint: float = 3.0):
 
 
 # ---------------------------------------------------------------------------
+# secondary lines (rank 0, N = 1): config 3 (K0) and the implicit-grid API
+# ---------------------------------------------------------------------------
+
+def secondary_config3(hbm_peak: float):
+    """K0 over the 100k-kernel corpus (config 3): instructions/s and HBM
+    roofline (4 B/instruction + 8 B offset + 144 B output per kernel)."""
+    import torch
+    from paper_1701_08547_b200 import _lib, batch, workloads
+    c = workloads.make_corpus(100_000)
+    rec = workloads.corpus_records(c)
+    lut = workloads.corpus_signature_lut()
+    d_rec, d_off = batch._to_device(rec), batch._to_device(c.offsets)
+    d_lut = batch._to_device(lut)
+    out = batch._empty(c.n_kernels * _lib.MIX.itemsize)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")   # > L2 (126 MB)
+    for _ in range(3):
+        batch.mix_reduce(d_rec, d_off, c.n_kernels, d_lut, len(lut), d_out=out)
+    ts = []
+    for _ in range(10):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        batch.mix_reduce(d_rec, d_off, c.n_kernels, d_lut, len(lut), d_out=out)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = statistics.median(ts)
+    byts = 4 * c.n_instr + 8 * (c.n_kernels + 1) + 144 * c.n_kernels
+    gbs = byts / (ms / 1e3) / 1e9
+    return {"workload": "config3-100k-kernel-sass-corpus", "kernels": c.n_kernels,
+            "instructions": c.n_instr, "value": c.n_instr / (ms / 1e3),
+            "unit": "instructions/s", "kernels_per_s": c.n_kernels / (ms / 1e3),
+            "ms": ms, "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak,
+                                   "unit": "GB/s", "frac": gbs / hbm_peak,
+                                   "algorithmic_bytes": byts},
+            "l2": "512 MB buffer written between launches (flush)"}
+
+
+def secondary_space_api(cfg, mode: str, steps: int = 5):
+    """score_space() from host TuningSpace objects: the implicit-grid scorer
+    (K2i) decodes every candidate from its index; per call the host packs
+    the space description, H2D-copies it and reads the top-k back."""
+    import torch
+    from paper_1701_08547_b200 import ScorePlan, score_space
+    plan = ScorePlan(cfg.kernels, cfg.archs, mode, k=cfg.k)
+    for _ in range(3):
+        plan.score_implicit()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        plan.score_implicit()
+    e1.record()
+    torch.cuda.synchronize()
+    k_ms = e0.elapsed_time(e1) / steps
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        score_space(cfg.kernels, cfg.archs, mode, cfg.k)
+    api_ms = (time.perf_counter() - t0) / steps * 1e3
+    return {"kernel": "score_space_kernel (K2i, implicit grid)", "kernel_ms": k_ms,
+            "kernel_value": plan.total / (k_ms / 1e3),
+            "api_ms": api_ms, "api_value": plan.total / (api_ms / 1e3), "unit": UNIT,
+            "note": "no candidate records in HBM; api_ms is wall time of score_space() "
+                    "including ScorePlan construction (K1 + feature table) and decode"}
+
+
+# ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
 
@@ -196,6 +263,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=4_000_000)
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-secondary", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -344,6 +412,15 @@ def main():
         except Exception as exc:  # keep the main number; say why e2e is missing
             e2e = {"value": None, "unit": UNIT, "error": repr(exc)[:300]}
 
+    secondary = None
+    if rank == 0 and world == 1 and not args.no_secondary:
+        secondary = {}
+        for name, fn in (("config3_mix_reduce", lambda: secondary_config3(hbm_peak)),
+                         ("implicit_grid_score_space", lambda: secondary_space_api(cfg, args.mode))):
+            try:
+                secondary[name] = fn()
+            except Exception as exc:
+                secondary[name] = {"error": repr(exc)[:200]}
     cpu = None
     c_oracle = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -372,6 +449,8 @@ def main():
                          "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src},
             "e2e": e2e, "gpu_launches": launches, "clocks": sampler.summary(),
         }
+        if secondary is not None:
+            line["secondary"] = secondary
         if cpu is not None:
             line["cpu_baseline"] = cpu
             line["cpu_oracle_c"] = c_oracle

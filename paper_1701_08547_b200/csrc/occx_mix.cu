@@ -98,27 +98,29 @@ __global__ void __launch_bounds__(kMixThreads) mix_reduce_kernel(const __grid_co
   const uint32_t warps_total = gridDim.x * (kMixThreads / 32);
   for (uint32_t kern = blockIdx.x * (kMixThreads / 32) + (threadIdx.x >> 5); kern < p.n_kernels;
        kern += warps_total) {
-    const uint64_t beg = p.off[kern], end = p.off[kern + 1];
+    const uint64_t beg = __ldg(p.off + kern), end = __ldg(p.off + kern + 1);
     uint32_t w[4] = {0, 0, 0, 0};     // 16 byte counters
     uint32_t total = 0;               // lane c < 16 holds counts[c]
     uint32_t first = kAbsent;         // lane c holds first_key[c]; lane 16 guard-PredIns
     uint32_t regs = 0;
     uint32_t warp_seen = 0;
     int since_flush = 0;
+    const uint32_t len = (uint32_t)min(end - beg, (uint64_t)0x7fffffff);
+    const uint32_t* src = p.instr + beg;
     uint32_t rec[kMixPer];
 #pragma unroll
     for (int u = 0; u < kMixPer; ++u) {
-      const uint64_t i = beg + (uint64_t)u * 32 + lane;
-      rec[u] = (i < end) ? __ldcs(p.instr + i) : null_rec;
+      const uint32_t i = (uint32_t)u * 32 + lane;
+      rec[u] = (i < len) ? __ldcs(src + i) : null_rec;
     }
-    for (uint64_t base = beg; base < end; base += 32 * kMixPer) {
+    for (uint32_t rb = 0; rb < len; rb += 32 * kMixPer) {
       // prefetch the next chunk while this one is processed
       uint32_t nxt[kMixPer];
-      const uint64_t nb = base + 32 * kMixPer;
+      const uint32_t nb = rb + 32 * kMixPer;
 #pragma unroll
       for (int u = 0; u < kMixPer; ++u) {
-        const uint64_t i = nb + (uint64_t)u * 32 + lane;
-        nxt[u] = (i < end) ? __ldcs(p.instr + i) : null_rec;
+        const uint32_t i = nb + (uint32_t)u * 32 + lane;
+        nxt[u] = (i < len) ? __ldcs(src + i) : null_rec;
       }
       uint32_t bits[kMixPer], seen = 0;
 #pragma unroll
@@ -140,21 +142,18 @@ __global__ void __launch_bounds__(kMixThreads) mix_reduce_kernel(const __grid_co
       uint32_t fresh = chunk_seen & ~warp_seen;
       if (fresh) {
         warp_seen |= chunk_seen;
-        // walk the slots in order: a class first seen in slot u gets one
-        // ballot over that slot (all warp-uniform except the ballot)
-        uint32_t left = fresh;
+        // first position of each new class: the lane's earliest slot, then
+        // one REDUX.MIN over the warp (positions are distinct)
+        const uint32_t rel0 = rb + (uint32_t)lane;
+        while (fresh) {
+          const uint32_t bt = __ffs(fresh) - 1;
+          fresh &= fresh - 1;
+          uint32_t mine = kAbsent;
 #pragma unroll
-        for (int u = 0; u < kMixPer; ++u) {
-          uint32_t f = left & __reduce_or_sync(0xffffffffu, bits[u]);
-          left &= ~f;
-          while (f) {
-            const uint32_t b = __ffs(f) - 1;
-            f &= f - 1;
-            const unsigned m = __ballot_sync(0xffffffffu, (bits[u] >> b) & 1u);
-            const uint32_t pos = (uint32_t)(base - beg) + (uint32_t)u * 32 + (__ffs(m) - 1);
-            if (lane == (int)b) first = 2u * pos + (b == 16 ? 1u : 0u);
-          }
-          if (left == 0) break;
+          for (int u = kMixPer - 1; u >= 0; --u)
+            if ((bits[u] >> bt) & 1u) mine = rel0 + (uint32_t)u * 32;
+          const uint32_t pos = __reduce_min_sync(0xffffffffu, mine);
+          if (lane == (int)bt) first = 2u * pos + (bt == 16 ? 1u : 0u);
         }
       }
       if (++since_flush == kFlushChunks) {
