@@ -352,6 +352,8 @@ struct IgCache {
   uint32_t n_s, r_off, s_off;
   FastDiv ds;
   uint32_t x, z, w_hi;   // record words: variant, T | BC << 16, arch << 16 | PL << 24
+  uint32_t seg;          // segment descriptor index
+  uint32_t d_cf, d_pl, d_uif, d_bc, d_tc;   // block digits (enumerate_space order)
 };
 
 struct SpaceParams {
@@ -362,6 +364,17 @@ struct SpaceParams {
   uint64_t begin;        // global index of the first candidate scored
 };
 
+// Record words of the block the digits point at.
+__device__ __forceinline__ void ig_derive(const SpaceParams& q, const uint32_t* pool, IgCache& c) {
+  const occx_segdesc_t* d = q.desc + c.seg;
+  const uint32_t T = pool[__ldg(&d->dim_off[0]) + c.d_tc];
+  const uint32_t B = pool[__ldg(&d->dim_off[1]) + c.d_bc];
+  c.x = __ldg(&d->var_base) + c.d_uif * __ldg(&d->dim_len[4]) + c.d_cf;
+  c.z = min(T, 0xffffu) | (min(B, 0xffffu) << 16);
+  c.w_hi = ((__ldg(&d->arch) & 0xffu) << 16) | ((c.d_pl & 0xffu) << 24);
+}
+
+// Full decode of g (binary search + divisions): warp start / segment change.
 __device__ __noinline__ void ig_fill(const SpaceParams& q, const uint32_t* pool, uint64_t g,
                                      IgCache& c) {
   uint32_t lo = 0, hi = q.n_desc;                      // last segment with start <= g
@@ -371,32 +384,59 @@ __device__ __noinline__ void ig_fill(const SpaceParams& q, const uint32_t* pool,
   }
   const occx_segdesc_t* d = q.desc + lo;
   const uint64_t start = __ldg(&d->start);
-  uint32_t off[7], len[7];
+  uint32_t len[7];
 #pragma unroll
-  for (int i = 0; i < 7; ++i) {
-    off[i] = __ldg(&d->dim_off[i]);
-    len[i] = __ldg(&d->dim_len[i]);
-  }
+  for (int i = 0; i < 7; ++i) len[i] = __ldg(&d->dim_len[i]);
   const uint64_t blk = (uint64_t)len[5] * len[6];
   uint64_t o = (g - start) / blk;
   c.blk_lo = start + o * blk;
   c.blk_n = (uint32_t)blk;
-  const uint32_t i_cf = (uint32_t)(o % len[4]);
+  c.d_cf = (uint32_t)(o % len[4]);
   o /= len[4];
-  const uint32_t i_pl = (uint32_t)(o % len[3]);
+  c.d_pl = (uint32_t)(o % len[3]);
   o /= len[3];
-  const uint32_t i_uif = (uint32_t)(o % len[2]);
+  c.d_uif = (uint32_t)(o % len[2]);
   o /= len[2];
-  const uint32_t i_bc = (uint32_t)(o % len[1]);
-  const uint32_t i_tc = (uint32_t)(o / len[1]);
-  const uint32_t T = pool[off[0] + i_tc], B = pool[off[1] + i_bc];
-  c.x = __ldg(&d->var_base) + i_uif * len[4] + i_cf;
-  c.z = min(T, 0xffffu) | (min(B, 0xffffu) << 16);
-  c.w_hi = ((__ldg(&d->arch) & 0xffu) << 16) | ((i_pl & 0xffu) << 24);
+  c.d_bc = (uint32_t)(o % len[1]);
+  c.d_tc = (uint32_t)(o / len[1]);
+  c.seg = lo;
   c.n_s = len[6];
-  c.r_off = off[5];
-  c.s_off = off[6];
+  c.r_off = __ldg(&d->dim_off[5]);
+  c.s_off = __ldg(&d->dim_off[6]);
   c.ds = fastdiv_make(len[6]);
+  ig_derive(q, pool, c);
+}
+
+// Step to the next block of the same segment (digit carry); false at the
+// segment's end.
+__device__ __forceinline__ bool ig_advance(const SpaceParams& q, const uint32_t* pool,
+                                           IgCache& c) {
+  const occx_segdesc_t* d = q.desc + c.seg;
+  if (++c.d_cf == __ldg(&d->dim_len[4])) {
+    c.d_cf = 0;
+    if (++c.d_pl == __ldg(&d->dim_len[3])) {
+      c.d_pl = 0;
+      if (++c.d_uif == __ldg(&d->dim_len[2])) {
+        c.d_uif = 0;
+        if (++c.d_bc == __ldg(&d->dim_len[1])) {
+          c.d_bc = 0;
+          if (++c.d_tc == __ldg(&d->dim_len[0])) return false;
+        }
+      }
+    }
+  }
+  c.blk_lo += c.blk_n;
+  ig_derive(q, pool, c);
+  return true;
+}
+
+// Make the cache cover g (g >= the cache's block start: warps walk forward).
+__device__ __forceinline__ void ig_seek(const SpaceParams& q, const uint32_t* pool, uint64_t g,
+                                        IgCache& c) {
+  const uint64_t off = g - c.blk_lo;
+  if (off < c.blk_n) return;
+  if (c.blk_n != 0 && off < 2ull * c.blk_n && ig_advance(q, pool, c)) return;
+  ig_fill(q, pool, g, c);
 }
 
 __device__ __forceinline__ uint4 ig_record(const IgCache& c, const uint32_t* pool, uint64_t g) {
@@ -407,8 +447,11 @@ __device__ __forceinline__ uint4 ig_record(const IgCache& c, const uint32_t* poo
   return make_uint4(c.x, S, c.z, min(R, 0xffffu) | c.w_hi);
 }
 
+constexpr int kIgThreads = 768;                 // 24 warps, one CTA per SM (<= 80 registers)
+constexpr int kIgWarps = kIgThreads / 32;
+
 template <int MODE, bool VT_SMEM>
-__global__ void __launch_bounds__(kLdgThreads, 2) score_space_kernel(const __grid_constant__ SpaceParams q) {
+__global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid_constant__ SpaceParams q) {
   extern __shared__ __align__(128) unsigned char smem[];
   const ScoreParams& p = q.sp;
   const K2Shared s = k2_setup<MODE, VT_SMEM>(p, smem);
@@ -425,7 +468,6 @@ __global__ void __launch_bounds__(kLdgThreads, 2) score_space_kernel(const __gri
   const uint64_t begin = q.begin + (uint64_t)blockIdx.x * p.chunk;
   const uint64_t stop = q.begin + p.n;
   const uint64_t end = begin + p.chunk < stop ? begin + p.chunk : stop;
-  constexpr int kTile = kLdgThreads * 4;
   WarpList wl{0, 0, kNoSeg};
   K2Cache cc;
   cc.x = cc.z = cc.w = 0xffffffffu;
@@ -433,35 +475,39 @@ __global__ void __launch_bounds__(kLdgThreads, 2) score_space_kernel(const __gri
   IgCache ic;
   ic.blk_lo = 0;
   ic.blk_n = 0;
-  const uint32_t slice = (threadIdx.x >> 5) * 128u + lane;
-  for (uint64_t base = begin; base < end; base += kTile) {
-    const uint64_t g0 = base + slice;
+  // each warp walks its own contiguous range in 128-candidate slices, so a
+  // lane's block advances by +1 (digit carry) instead of being re-decoded
+  const uint64_t wsz = p.chunk / kIgWarps;               // multiple of 128
+  const uint64_t wb = begin + (threadIdx.x >> 5) * wsz;
+  const uint64_t we = wb + wsz < end ? wb + wsz : end;
+  for (uint64_t base = wb; base < we; base += 128) {
+    const uint64_t g0 = base + lane;
+    uint4 r[4];
     bool hit = true;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const uint64_t g = g0 + 32u * j;
-      hit &= (g >= end) || (g - ic.blk_lo < (uint64_t)ic.blk_n);
+      hit &= (g >= we) || (g - ic.blk_lo < (uint64_t)ic.blk_n);
     }
-    uint4 r[4];
-    if (__all_sync(0xffffffffu, hit)) {
+    if (!__all_sync(0xffffffffu, hit)) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const uint64_t g = g0 + 32u * j;
-        r[j] = g < end ? ig_record(ic, pool, g) : make_uint4(0, 0, 0, 0xffffffffu);
+        if (g < we) ig_seek(q, pool, g, ic);
+        r[j] = g < we ? ig_record(ic, pool, g) : make_uint4(0, 0, 0, 0xffffffffu);
       }
     } else {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const uint64_t g = g0 + 32u * j;
-        if (g < end && !(g - ic.blk_lo < (uint64_t)ic.blk_n)) ig_fill(q, pool, g, ic);
-        r[j] = g < end ? ig_record(ic, pool, g) : make_uint4(0, 0, 0, 0xffffffffu);
+        r[j] = g < we ? ig_record(ic, pool, g) : make_uint4(0, 0, 0, 0xffffffffu);
       }
     }
     k2_process4<MODE, VT_SMEM>(s, cc, wl, r, kIdxMask - g0, lane, p.k);
   }
   k2_stage(wl, lane, p.k, stage, threadIdx.x >> 5);
   __syncthreads();
-  if (threadIdx.x < 32) k2_merge_staged(stage, kLdgThreads / 32, p.k, s.thr, s.list, s.lock);
+  if (threadIdx.x < 32) k2_merge_staged(stage, kIgWarps, p.k, s.thr, s.list, s.lock);
   __syncthreads();
   k2_flush(p, s);
 }
@@ -1041,8 +1087,8 @@ extern "C" int occx_score_space(const occx_ctx* ctx, const occx_arch_t* h_archs,
   q.n_desc = n_desc;
   q.n_pool = n_pool;
   q.begin = begin;
-  const int grid = score_grid(ctx);
-  const uint64_t tile = (uint64_t)kLdgThreads * 4;
+  const int grid = ctx->sm_count;                         // one 768-thread CTA per SM
+  const uint64_t tile = (uint64_t)kIgWarps * 128;          // each warp walks chunk / kIgWarps
   const uint64_t tiles = (n + tile - 1) / tile;
   q.sp.chunk = ((tiles + grid - 1) / grid) * tile;
   if (q.sp.chunk == 0) q.sp.chunk = tile;
@@ -1055,7 +1101,7 @@ extern "C" int occx_score_space(const occx_ctx* ctx, const occx_arch_t* h_archs,
 #define OCCX_LAUNCH_IG(KERNEL)                                                       \
   do {                                                                               \
     if (set_smem(KERNEL, smem)) return OCCX_ERR_CUDA;                                \
-    KERNEL<<<grid, kLdgThreads, smem, s>>>(q);                                       \
+    KERNEL<<<grid, kIgThreads, smem, s>>>(q);                                        \
   } while (0)
   const bool vts = q.sp.vt_smem != 0;
   if (mode == OCCX_MODE_CORRECTED) {
