@@ -8,12 +8,13 @@
 //       counts[PredIns] += 1        CATEGORY_OF.get(UNCLASSIFIED) is None)
 //   reg_operands += regops         mix.py:260
 //
-// Counting: each lane keeps sixteen 8-bit counters packed in four u32
-// registers.  A second 32-entry table indexed by (class | guard << 4) holds
-// the 16-byte increment vector of each case (the class byte, plus the
-// PredIns byte when the guard counts), so a record costs one LDS.U8, one
-// LDS.128 and four IADDs.  Counters are reduced with 16-bit-lane REDUX.SUM
-// (bytes 0/2 and 1/3 separately) before they can overflow.
+// Counting: a 32-entry table indexed by (class | guard << 4) holds the u64
+// increment of each case over sixteen 4-bit counters (class nibble, plus
+// the PredIns nibble and a "guard counted" marker in the spare nibble 15
+// when the guard adds a PredIns), so a record costs one LDS.U8, one LDS.64
+// and a 64-bit add.  Each chunk of 8 records per lane is folded into two
+// u64 byte-counter words (even / odd classes), reduced over the warp with
+// 16-bit-lane REDUX.SUM before they can overflow.
 // Dict insertion order (it decides the summation order of the FLOPS terms
 // in mix.py:278) is recovered as first_key[c] = min over occurrences of
 // 2*i (class of instruction i) or 2*i+1 (guard PredIns of instruction i);
@@ -27,7 +28,7 @@ namespace {
 
 constexpr int kMixThreads = 256;
 constexpr int kMixPer = 8;                            // records per lane per chunk
-constexpr int kFlushChunks = 255 / (2 * kMixPer);     // byte counters cannot overflow
+constexpr int kFlushChunks = 255 / kMixPer;           // byte counters cannot overflow
 constexpr uint32_t kPred = 11;                        // OpClass.PREDICATE device id
 constexpr uint32_t kAbsent = 0xffffffffu;
 constexpr uint32_t kNullClass = 15;                   // padding record: counts nothing
@@ -46,52 +47,46 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
   asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
-__device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
-  uint4 v;
-  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "r"(addr));
-  return v;
-}
 
-// Sum the 16 packed byte counters over the warp; lane c < 16 receives
-// class c's total.  Bytes 0/2 and 1/3 are reduced in separate 16-bit lanes
-// (32 x 255 < 2^16), 8 REDUX.SUM for 16 counters.
-__device__ __forceinline__ void reduce_counters(const uint32_t (&w)[4], int lane,
-                                                uint32_t& total) {
+// Sum 16 byte counters held as even classes (w[0] classes 0,2,4,6; w[1]
+// 8,10,12,14) and odd classes (w[2] 1,3,5,7; w[3] 9,11,13,15); lane c < 16
+// receives class c's total.  16-bit lanes: 32 x 255 < 2^16.
+__device__ __forceinline__ void reduce_counters_eo(const uint32_t (&w)[4], int lane,
+                                                   uint32_t& total) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const uint32_t even = __reduce_add_sync(0xffffffffu, w[q] & 0x00ff00ffu);
-    const uint32_t odd = __reduce_add_sync(0xffffffffu, (w[q] >> 8) & 0x00ff00ffu);
-    const int c = 4 * q;
-    if (lane == c) total += even & 0xffffu;
-    if (lane == c + 1) total += odd & 0xffffu;
-    if (lane == c + 2) total += even >> 16;
-    if (lane == c + 3) total += odd >> 16;
+    const uint32_t lo = __reduce_add_sync(0xffffffffu, w[q] & 0x00ff00ffu);   // bytes 0, 2
+    const uint32_t hi = __reduce_add_sync(0xffffffffu, (w[q] >> 8) & 0x00ff00ffu);  // bytes 1, 3
+    const int base = (q & 1) * 8 + (q >> 1);             // class of byte 0 in this word
+    if (lane == base) total += lo & 0xffffu;
+    if (lane == base + 2) total += hi & 0xffffu;
+    if (lane == base + 4) total += lo >> 16;
+    if (lane == base + 6) total += hi >> 16;
   }
 }
 
 __global__ void __launch_bounds__(kMixThreads) mix_reduce_kernel(const __grid_constant__ MixParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
-  uint4* inc = reinterpret_cast<uint4*>(smem);              // [32] increment vectors
-  unsigned char* lut = smem + 32 * sizeof(uint4);           // [n_sig + 1] class ids
+  // [32] u64 nibble increments, [warps][17] first positions, [n_sig + 1] class LUT
+  uint64_t* inc = reinterpret_cast<uint64_t*>(smem);
+  uint32_t* firsts = reinterpret_cast<uint32_t*>(inc + 32);
+  unsigned char* lut = reinterpret_cast<unsigned char*>(firsts + (kMixThreads / 32) * 17 + 2);
   for (uint32_t i = threadIdx.x; i < 32; i += blockDim.x) {
     const uint32_t c = i & 15u, g = i >> 4;
-    uint32_t v[4] = {0, 0, 0, 0};
+    uint64_t v = 0;
     if (c < 15) {
-      v[c >> 2] += 1u << ((c & 3) * 8);
-      if (g && !(c >= 11 && c <= 13)) {
-        v[kPred >> 2] += 1u << ((kPred & 3) * 8);
-        v[3] += 1u << 24;               // byte 15: "guard added a PredIns" marker
-      }
+      v = 1ull << (4 * c);
+      if (g && !(c >= 11 && c <= 13)) v += (1ull << (4 * kPred)) + (1ull << 60);  // PredIns + marker
     }
-    inc[i] = make_uint4(v[0], v[1], v[2], v[3]);
+    inc[i] = v;
   }
+  for (uint32_t i = threadIdx.x; i < (kMixThreads / 32) * 17; i += blockDim.x) firsts[i] = kAbsent;
   for (uint32_t i = threadIdx.x; i <= p.n_sig; i += blockDim.x)
     lut[i] = i < p.n_sig ? (uint8_t)(p.sig_class[i] & 15u) : (uint8_t)kNullClass;
   __syncthreads();
   const uint32_t inc_base = (uint32_t)__cvta_generic_to_shared(inc);
   const uint32_t lut_base = (uint32_t)__cvta_generic_to_shared(lut);
+  uint32_t* my_first = firsts + (threadIdx.x >> 5) * 17;
   const uint32_t null_rec = p.n_sig;                        // sig = n_sig -> class 15
 
   const int lane = threadIdx.x & 31;
@@ -99,12 +94,12 @@ __global__ void __launch_bounds__(kMixThreads) mix_reduce_kernel(const __grid_co
   for (uint32_t kern = blockIdx.x * (kMixThreads / 32) + (threadIdx.x >> 5); kern < p.n_kernels;
        kern += warps_total) {
     const uint64_t beg = __ldg(p.off + kern), end = __ldg(p.off + kern + 1);
-    uint32_t w[4] = {0, 0, 0, 0};     // 16 byte counters
-    uint32_t total = 0;               // lane c < 16 holds counts[c]
-    uint32_t first = kAbsent;         // lane c holds first_key[c]; lane 16 guard-PredIns
+    // byte counters: even classes (0,2,..,14) and odd classes (1,3,..,15)
+    uint64_t b_even = 0, b_odd = 0;
+    uint32_t seen_lo = 0, seen_hi = 0;                      // nibble-presence seen so far
     uint32_t regs = 0;
-    uint32_t warp_seen = 0;
     int since_flush = 0;
+    uint32_t total = 0;
     const uint32_t len = (uint32_t)min(end - beg, (uint64_t)0x7fffffff);
     const uint32_t* src = p.instr + beg;
     uint32_t rec[kMixPer];
@@ -114,59 +109,69 @@ __global__ void __launch_bounds__(kMixThreads) mix_reduce_kernel(const __grid_co
       rec[u] = (i < len) ? __ldcs(src + i) : null_rec;
     }
     for (uint32_t rb = 0; rb < len; rb += 32 * kMixPer) {
-      // prefetch the next chunk while this one is processed
-      uint32_t nxt[kMixPer];
+      uint32_t nxt[kMixPer];                               // prefetch the next chunk
       const uint32_t nb = rb + 32 * kMixPer;
 #pragma unroll
       for (int u = 0; u < kMixPer; ++u) {
         const uint32_t i = nb + (uint32_t)u * 32 + lane;
         nxt[u] = (i < len) ? __ldcs(src + i) : null_rec;
       }
-      uint32_t bits[kMixPer], seen = 0;
+      uint64_t v = 0;                                      // this chunk's 4-bit counters
+      uint32_t idxs[kMixPer];
 #pragma unroll
       for (int u = 0; u < kMixPer; ++u) {
         const uint32_t r = rec[u];
         const uint32_t c = lds_u8(lut_base + (r & 0xffffu));
-        const uint32_t idx = c | ((r >> 20) & 16u);          // guard bit 24 -> bit 4
-        const uint4 d = lds_v4(inc_base + idx * 16u);
-        w[0] += d.x;
-        w[1] += d.y;
-        w[2] += d.z;
-        w[3] += d.w;
+        const uint32_t idx = c | ((r >> 20) & 16u);         // guard bit 24 -> bit 4
+        uint64_t d;
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(d) : "r"(inc_base + idx * 8u));
+        v += d;
         regs += __byte_perm(r, 0, 0x4442);                  // register operands (byte 2)
-        // class bit (bit 15 = padding, masked below) + guard-PredIns at bit 16
-        bits[u] = (1u << c) | ((d.w >> 24) << 16);
-        seen |= bits[u];
+        idxs[u] = idx;
       }
-      const uint32_t chunk_seen = __reduce_or_sync(0xffffffffu, seen) & 0x17fffu;
-      uint32_t fresh = chunk_seen & ~warp_seen;
-      if (fresh) {
-        warp_seen |= chunk_seen;
-        // first position of each new class: the lane's earliest slot, then
-        // one REDUX.MIN over the warp (positions are distinct)
-        const uint32_t rel0 = rb + (uint32_t)lane;
-        while (fresh) {
-          const uint32_t bt = __ffs(fresh) - 1;
-          fresh &= fresh - 1;
-          uint32_t mine = kAbsent;
+      // classes (nibbles) present in this lane's chunk -> warp presence
+      uint64_t t = v | (v >> 1);
+      t |= t >> 2;
+      t &= 0x1111111111111111ull;
+      const uint32_t pres_lo = __reduce_or_sync(0xffffffffu, (uint32_t)t);
+      const uint32_t pres_hi = __reduce_or_sync(0xffffffffu, (uint32_t)(t >> 32)) & 0x1fffffffu;
+      if ((pres_lo & ~seen_lo) | (pres_hi & ~seen_hi)) {   // a class new to this kernel
+        seen_lo |= pres_lo;
+        seen_hi |= pres_hi;
 #pragma unroll
-          for (int u = kMixPer - 1; u >= 0; --u)
-            if ((bits[u] >> bt) & 1u) mine = rel0 + (uint32_t)u * 32;
-          const uint32_t pos = __reduce_min_sync(0xffffffffu, mine);
-          if (lane == (int)bt) first = 2u * pos + (bt == 16 ? 1u : 0u);
+        for (int u = 0; u < kMixPer; ++u) {
+          const uint32_t c = idxs[u] & 15u;
+          const uint32_t pos = rb + (uint32_t)u * 32 + lane;
+          if (c != kNullClass) {
+            atomicMin(my_first + c, 2u * pos);
+            // guard PredIns (non-CTRL class): key 2*pos + 1, tracked in slot 16
+            if ((idxs[u] & 16u) && !(c >= 11 && c <= 13)) atomicMin(my_first + 16, 2u * pos + 1);
+          }
         }
       }
+      b_even += v & 0x0f0f0f0f0f0f0f0full;
+      b_odd += (v >> 4) & 0x0f0f0f0f0f0f0f0full;
       if (++since_flush == kFlushChunks) {
         since_flush = 0;
-        reduce_counters(w, lane, total);
-        w[0] = w[1] = w[2] = w[3] = 0;
+        const uint32_t w[4] = {(uint32_t)b_even, (uint32_t)(b_even >> 32), (uint32_t)b_odd,
+                               (uint32_t)(b_odd >> 32)};
+        reduce_counters_eo(w, lane, total);
+        b_even = b_odd = 0;
       }
 #pragma unroll
       for (int u = 0; u < kMixPer; ++u) rec[u] = nxt[u];
     }
-    reduce_counters(w, lane, total);
+    {
+      const uint32_t w[4] = {(uint32_t)b_even, (uint32_t)(b_even >> 32), (uint32_t)b_odd,
+                             (uint32_t)(b_odd >> 32)};
+      reduce_counters_eo(w, lane, total);
+    }
+    __syncwarp();
+    uint32_t first = lane < 17 ? my_first[lane] : kAbsent;
     const uint32_t gfirst = __shfl_sync(0xffffffffu, first, 16);
     if (lane == (int)kPred && gfirst < first) first = gfirst;
+    if (lane < 17) my_first[lane] = kAbsent;               // reset for the warp's next kernel
+    __syncwarp();
     const uint32_t reg_total = __reduce_add_sync(0xffffffffu, regs);
     occx_mix_t* o = p.out + kern;
     if (lane < 16) {
@@ -196,7 +201,7 @@ extern "C" int occx_mix_reduce(const occx_ctx* ctx, const uint32_t* d_instr,
   p.sig_class = d_sig_class;
   p.n_sig = n_sig;
   p.out = d_out;
-  const size_t smem = 32 * 16 + ((n_sig + 1 + 15) & ~15u);
+  const size_t smem = 32 * 8 + ((kMixThreads / 32) * 17 + 2) * 4 + ((n_sig + 1 + 15) & ~15u);
   if (smem > 48 * 1024 &&
       cudaFuncSetAttribute(mix_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)
