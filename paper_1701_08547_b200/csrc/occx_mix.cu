@@ -91,79 +91,108 @@ __global__ void __launch_bounds__(kMixThreads) mix_reduce_kernel(const __grid_co
 
   const int lane = threadIdx.x & 31;
   const uint32_t warps_total = gridDim.x * (kMixThreads / 32);
-  for (uint32_t kern = blockIdx.x * (kMixThreads / 32) + (threadIdx.x >> 5); kern < p.n_kernels;
-       kern += warps_total) {
-    const uint64_t beg = __ldg(p.off + kern), end = __ldg(p.off + kern + 1);
-    // byte counters: even classes (0,2,..,14) and odd classes (1,3,..,15)
-    uint64_t b_even = 0, b_odd = 0;
-    uint32_t seen_lo = 0, seen_hi = 0;                      // nibble-presence seen so far
-    uint32_t regs = 0;
-    int since_flush = 0;
-    uint32_t total = 0;
+  uint32_t kern = blockIdx.x * (kMixThreads / 32) + (threadIdx.x >> 5);
+  // software pipeline across kernels: the next kernel's offsets and first
+  // chunk are loaded while the current kernel is being reduced
+  uint64_t beg = 0, end = 0;
+  if (kern < p.n_kernels) {
+    beg = __ldg(p.off + kern);
+    end = __ldg(p.off + kern + 1);
+  }
+  uint32_t rec[kMixPer];
+  {
     const uint32_t len = (uint32_t)min(end - beg, (uint64_t)0x7fffffff);
-    const uint32_t* src = p.instr + beg;
-    uint32_t rec[kMixPer];
 #pragma unroll
     for (int u = 0; u < kMixPer; ++u) {
       const uint32_t i = (uint32_t)u * 32 + lane;
-      rec[u] = (i < len) ? __ldcs(src + i) : null_rec;
+      rec[u] = (i < len) ? __ldcs(p.instr + beg + i) : null_rec;
     }
+  }
+  while (kern < p.n_kernels) {
+    const uint32_t nkern = kern + warps_total;
+    uint64_t nbeg = 0, nend = 0;
+    if (nkern < p.n_kernels) {
+      nbeg = __ldg(p.off + nkern);
+      nend = __ldg(p.off + nkern + 1);
+    }
+    const uint32_t nlen = (uint32_t)min(nend - nbeg, (uint64_t)0x7fffffff);
+    const uint32_t len = (uint32_t)min(end - beg, (uint64_t)0x7fffffff);
+    const uint32_t* src = p.instr + beg;
+    // byte counters: even classes (0,2,..,14) and odd classes (1,3,..,15)
+    uint32_t be0 = 0, be1 = 0, bo0 = 0, bo1 = 0;
+    uint32_t seen_lo = 0, seen_hi = 0;                      // nibble presence so far
+    uint32_t regs = 0, total = 0;
+    int since_flush = 0;
+    uint32_t nxt[kMixPer];
     for (uint32_t rb = 0; rb < len; rb += 32 * kMixPer) {
-      uint32_t nxt[kMixPer];                               // prefetch the next chunk
       const uint32_t nb = rb + 32 * kMixPer;
+      if (nb < len) {                                      // next chunk of this kernel
 #pragma unroll
-      for (int u = 0; u < kMixPer; ++u) {
-        const uint32_t i = nb + (uint32_t)u * 32 + lane;
-        nxt[u] = (i < len) ? __ldcs(src + i) : null_rec;
+        for (int u = 0; u < kMixPer; ++u) {
+          const uint32_t i = nb + (uint32_t)u * 32 + lane;
+          nxt[u] = (i < len) ? __ldcs(src + i) : null_rec;
+        }
+      } else {                                             // first chunk of the next kernel
+#pragma unroll
+        for (int u = 0; u < kMixPer; ++u) {
+          const uint32_t i = (uint32_t)u * 32 + lane;
+          nxt[u] = (i < nlen) ? __ldcs(p.instr + nbeg + i) : null_rec;
+        }
       }
-      uint64_t v = 0;                                      // this chunk's 4-bit counters
-      uint32_t idxs[kMixPer];
+      uint32_t v0 = 0, v1 = 0;                             // 4-bit counters, classes 0-7 / 8-15
 #pragma unroll
       for (int u = 0; u < kMixPer; ++u) {
         const uint32_t r = rec[u];
         const uint32_t c = lds_u8(lut_base + (r & 0xffffu));
         const uint32_t idx = c | ((r >> 20) & 16u);         // guard bit 24 -> bit 4
-        uint64_t d;
-        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(d) : "r"(inc_base + idx * 8u));
-        v += d;
+        uint32_t d0, d1;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(d0), "=r"(d1) : "r"(inc_base + idx * 8u));
+        v0 += d0;
+        v1 += d1;
         regs += __byte_perm(r, 0, 0x4442);                  // register operands (byte 2)
-        idxs[u] = idx;
       }
       // classes (nibbles) present in this lane's chunk -> warp presence
-      uint64_t t = v | (v >> 1);
-      t |= t >> 2;
-      t &= 0x1111111111111111ull;
-      const uint32_t pres_lo = __reduce_or_sync(0xffffffffu, (uint32_t)t);
-      const uint32_t pres_hi = __reduce_or_sync(0xffffffffu, (uint32_t)(t >> 32)) & 0x1fffffffu;
+      uint32_t t0 = v0 | (v0 >> 1), t1 = v1 | (v1 >> 1);
+      t0 = (t0 | (t0 >> 2)) & 0x11111111u;
+      t1 = (t1 | (t1 >> 2)) & 0x11111111u;
+      const uint32_t pres_lo = __reduce_or_sync(0xffffffffu, t0);
+      const uint32_t pres_hi = __reduce_or_sync(0xffffffffu, t1);
       if ((pres_lo & ~seen_lo) | (pres_hi & ~seen_hi)) {   // a class new to this kernel
         seen_lo |= pres_lo;
         seen_hi |= pres_hi;
 #pragma unroll
-        for (int u = 0; u < kMixPer; ++u) {
-          const uint32_t c = idxs[u] & 15u;
+        for (int u = 0; u < kMixPer; ++u) {                // rare: re-read the classes
+          const uint32_t c = lds_u8(lut_base + (rec[u] & 0xffffu));
           const uint32_t pos = rb + (uint32_t)u * 32 + lane;
           if (c != kNullClass) {
             atomicMin(my_first + c, 2u * pos);
             // guard PredIns (non-CTRL class): key 2*pos + 1, tracked in slot 16
-            if ((idxs[u] & 16u) && !(c >= 11 && c <= 13)) atomicMin(my_first + 16, 2u * pos + 1);
+            if (((rec[u] >> 24) & 1u) && !(c >= 11 && c <= 13)) atomicMin(my_first + 16, 2u * pos + 1);
           }
         }
       }
-      b_even += v & 0x0f0f0f0f0f0f0f0full;
-      b_odd += (v >> 4) & 0x0f0f0f0f0f0f0f0full;
+      be0 += v0 & 0x0f0f0f0fu;
+      bo0 += (v0 >> 4) & 0x0f0f0f0fu;
+      be1 += v1 & 0x0f0f0f0fu;
+      bo1 += (v1 >> 4) & 0x0f0f0f0fu;
       if (++since_flush == kFlushChunks) {
         since_flush = 0;
-        const uint32_t w[4] = {(uint32_t)b_even, (uint32_t)(b_even >> 32), (uint32_t)b_odd,
-                               (uint32_t)(b_odd >> 32)};
+        const uint32_t w[4] = {be0, be1, bo0, bo1};
         reduce_counters_eo(w, lane, total);
-        b_even = b_odd = 0;
+        be0 = be1 = bo0 = bo1 = 0;
       }
 #pragma unroll
       for (int u = 0; u < kMixPer; ++u) rec[u] = nxt[u];
     }
+    if (len == 0) {                                        // empty kernel: load the next chunk now
+#pragma unroll
+      for (int u = 0; u < kMixPer; ++u) {
+        const uint32_t i = (uint32_t)u * 32 + lane;
+        rec[u] = (i < nlen) ? __ldcs(p.instr + nbeg + i) : null_rec;
+      }
+    }
     {
-      const uint32_t w[4] = {(uint32_t)b_even, (uint32_t)(b_even >> 32), (uint32_t)b_odd,
-                             (uint32_t)(b_odd >> 32)};
+      const uint32_t w[4] = {be0, be1, bo0, bo1};
       reduce_counters_eo(w, lane, total);
     }
     __syncwarp();
@@ -183,6 +212,9 @@ __global__ void __launch_bounds__(kMixThreads) mix_reduce_kernel(const __grid_co
       o->n_instr = (uint32_t)(end - beg);
       o->reserved = 0;
     }
+    kern = nkern;
+    beg = nbeg;
+    end = nend;
   }
 }
 
