@@ -1,0 +1,159 @@
+"""Randomised GPU parity: random architecture tables (anything the packed
+device form can represent), random tuning spaces, random instruction mixes,
+both evaluation modes -- CUDA path vs the independent oracles.  Seeded, so
+a failure reproduces."""
+
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import pyref
+
+pytestmark = pytest.mark.gpu
+
+
+def random_arch(rng, i):
+    from paper_1701_08547_b200.arch import ArchSpec, Family
+    ws = rng.choice((8, 16, 32, 32, 32, 64))
+    wpb_max = rng.randint(1, 64)
+    tmax = ws * wpb_max
+    wmp = rng.randint(1, min(127, max(1, 4096 // ws)))
+    bmp = rng.randint(1, 255)
+    rfs = rng.choice((16384, 32768, 65536, 131072, rng.randint(1024, (1 << 20) - 1)))
+    gran = rng.choice((1, 2, 64, 128, 256, 512, rng.randint(1, 4096)))
+    rmax = rng.randint(1, min(1023, rfs))
+    smax = rng.choice((16384, 49152, 98304, 232448, rng.randint(1, (1 << 24) - 1)))
+    cc = rng.choice((2.0, 3.5, 3.7, 5.2, 6.0, 6.1, 7.0, 9.0, 10.0))
+    return ArchSpec(name=f"rand{i}", family=Family.OTHER, compute_capability=cc,
+                    multiprocessors=1, warp_size=ws, max_threads_per_mp=wmp * ws,
+                    max_threads_per_block=tmax, max_blocks_per_mp=bmp, max_warps_per_mp=wmp,
+                    register_file_size=rfs, register_alloc_granularity=gran,
+                    max_regs_per_thread=rmax, shared_mem_per_block=smax)
+
+
+def random_mix(rng):
+    from paper_1701_08547_b200.mix import COUNTABLE, InstructionMix
+    classes = list(COUNTABLE)
+    rng.shuffle(classes)
+    counts = {c: rng.randint(0, 400) for c in classes[:rng.randint(0, 10)]}
+    return InstructionMix(counts, rng.randint(0, 3000))
+
+
+def random_config(rng, n_arch=3, n_kern=3):
+    from paper_1701_08547_b200 import workloads
+    from paper_1701_08547_b200.batch import KernelSpec
+    from paper_1701_08547_b200.tuning import TuningSpace
+    archs = tuple(random_arch(rng, i) for i in range(n_arch))
+    kernels = []
+    for kk in range(n_kern):
+        tc = tuple(sorted(rng.sample(range(32, 2048, 32), rng.randint(1, 12))))   # masks: T < 2048
+        if rng.random() < 0.3:
+            tc = tuple(rng.sample(tc, len(tc)))                  # unsorted thread dimension
+        space = TuningSpace(tc, tuple(rng.sample(range(1, 300), rng.randint(1, 3))),
+                            tuple(range(1, rng.randint(2, 4))), (16, 48)[:rng.randint(1, 2)],
+                            ("", "-use_fast_math")[:rng.randint(1, 2)],
+                            extra=(("REGS", tuple(rng.sample(range(0, 1100), rng.randint(1, 9)))),
+                                   ("SMEM", tuple(rng.choice((0, 1, 1024, 6145, 49152, 232448,
+                                                              rng.randint(0, 1 << 25)))
+                                                  for _ in range(rng.randint(1, 6))))))
+        n_var = len(space.unroll_factors) * len(space.compiler_flags)
+        kernels.append(KernelSpec(f"k{kk}", space, tuple(random_mix(rng) for _ in range(n_var))))
+    return workloads.Config("random", tuple(kernels), archs, rng.choice((1, 3, 16, 32)))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_spaces_k2_k2i_vs_oracle(seed):
+    import paper_1701_08547_b200 as P
+    rng = random.Random(1000 + seed)
+    cfg = random_config(rng, n_arch=rng.randint(1, 4), n_kern=rng.randint(1, 4))
+    for mode in ("corrected", "verbatim"):
+        prob = oracle.problem_of(cfg, verbatim=mode == "verbatim")
+        want = oracle.score_spaces(prob, oracle.spaces_of(cfg), threads=4)
+        plan = P.ScorePlan(cfg.kernels, cfg.archs, mode, k=cfg.k)
+        rec = plan.generate()
+        got = plan.score(rec, plan.total).cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, want), (seed, mode)
+        got_i = plan.score_implicit().cpu().numpy().view(np.uint64)
+        assert np.array_equal(got_i, want), (seed, mode, "implicit")
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_archs_occupancy_vs_oracle(seed):
+    from paper_1701_08547_b200.batch import occupancy_batch
+    rng = random.Random(7 + seed)
+    archs = [random_arch(rng, i) for i in range(8)]
+    n = 200_000
+    T = np.array([rng.randint(0, 2200) for _ in range(n)])
+    R = np.array([rng.choice((0, rng.randint(0, 1100), rng.randint(0, 70000))) for _ in range(n)])
+    S = np.array([rng.choice((0, rng.randint(0, 1 << 24), rng.randint(0, 1 << 33)))
+                  for _ in range(n)])
+    A = np.array([rng.randrange(8) for _ in range(n)])
+    for mode in ("corrected", "verbatim"):
+        ob = occupancy_batch(archs, np.stack([T, R, S], 1), mode, arch_index=A)
+        o = oracle.occupancy_many(archs, A, T, np.minimum(R, 0xFFFF),
+                                  np.minimum(S, 0xFFFFFFFF), verbatim=mode == "verbatim")
+        illegal = o["status"] != 0
+        np.testing.assert_array_equal(ob.raw["status"] == 2, illegal)
+        ok = ~illegal
+        for f_gpu, f_or in (("wpb", "wpb"), ("limit_warps", "lw"), ("limit_regs", "lr"),
+                            ("limit_smem", "ls"), ("active_blocks", "blocks"),
+                            ("active_warps", "aw"), ("limiter", "limiter"),
+                            ("reg_warp_limit", "rwl")):
+            np.testing.assert_array_equal(ob.raw[f_gpu][ok].astype(np.int64), o[f_or][ok],
+                                          err_msg=f"{f_gpu} seed {seed} {mode}")
+        np.testing.assert_array_equal(ob.raw["occupancy"][ok].view(np.int64),
+                                      o["occ"][ok].view(np.int64))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_suggest_vs_oracle(seed):
+    import paper_1701_08547_b200 as P
+    from paper_1701_08547_b200.batch import suggest_batch
+    rng = random.Random(99 + seed)
+    archs = [random_arch(rng, i) for i in range(6)]
+    reqs, want = [], []
+    for _ in range(3000):
+        a = rng.choice(archs)
+        regs = rng.choice((0, rng.randint(0, a.max_regs_per_thread), a.max_regs_per_thread))
+        smem = rng.choice((0, rng.randint(0, a.shared_mem_per_block), a.shared_mem_per_block))
+        if not pyref.thread_candidates(a):
+            continue
+        reqs.append((a, P.KernelResources("k", regs, smem)))
+        want.append(pyref.suggest(a, regs, smem))
+    for mode in ("corrected", "verbatim"):
+        if mode == "verbatim":
+            want = [pyref.suggest(a, r.registers_per_thread, r.static_shared_mem, True)
+                    for a, r in reqs]
+        got = suggest_batch(reqs, mode)
+        for g, w in zip(got, want):
+            assert (g.thread_candidates, g.register_headroom, g.smem_budget, g.best_occupancy,
+                    g.best_threads, g.best_blocks) == \
+                (w["thread_candidates"], w["register_headroom"], w["smem_budget"],
+                 w["best_occupancy"], w["best_threads"], w["best_blocks"])
+
+
+def test_random_mixes_features_vs_pyref():
+    from paper_1701_08547_b200.batch import feature_score
+    rng = random.Random(4242)
+    mixes = [random_mix(rng) for _ in range(2000)]
+    ccs = [2.0, 3.5, 5.2, 6.0, 6.1, 9.0]
+    for scale in (1.0, 0.1, 3.0):
+        fb = feature_score(mixes, ccs, scale=scale)
+        for m, mix in enumerate(mixes):
+            counts = {c.value: n for c, n in mix.counts.items()}
+            assert fb.intensity[m] == pyref.intensity(counts) or \
+                (np.isnan(fb.intensity[m]) and np.isnan(pyref.intensity(counts)))
+            for j, cc in enumerate(ccs):
+                try:
+                    want = pyref.cost_estimate(counts, mix.reg_operands, cc, scale)
+                except pyref.OracleUnsupported:
+                    with pytest.raises(Exception):
+                        fb.one(m, j)
+                    continue
+                got = fb.one(m, j)
+                assert got.cost.hex() == want.hex()
+                assert [x.hex() for x in got.shares.values()] == \
+                    [x.hex() for x in pyref.pipeline_utilization(counts, mix.reg_operands,
+                                                                 cc).values()]
