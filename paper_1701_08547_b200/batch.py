@@ -545,8 +545,9 @@ class ScorePlan:
     def score(self, d_records, n: int, index_base: int = 0, out=None, stream=None):
         """K2+K3 over n records in HBM -> device u64 [n_seg, k] top-k keys."""
         torch = _torch()
-        out = out if out is not None else torch.zeros((self.n_seg, self.k), dtype=torch.int64,
-                                                       device="cuda")
+        # K3 writes every entry of the [n_seg, k] table: no zero-fill needed
+        out = out if out is not None else torch.empty((self.n_seg, self.k), dtype=torch.int64,
+                                                      device="cuda")
         _lib.check(_lib.load().occx_score_topk(
             _lib.ctx(), _lib.ptr(self.h_archs), self.n_arch, _lib.ptr(d_records), n, index_base,
             MODE_CODE[self.mode], _lib.ptr(self.d_vtab), self.n_var, self.n_seg, self.k,
@@ -575,7 +576,7 @@ class ScorePlan:
         if getattr(self, "_stage", None) is None or self._stage[0].numel() < chunk * 16:
             self._stage = [_empty(chunk * 16), _empty(chunk * 16)]
         n_chunks = max(1, -(-n // chunk))
-        tables = torch.zeros((n_chunks, self.n_seg, self.k), dtype=torch.int64, device="cuda")
+        tables = torch.empty((n_chunks, self.n_seg, self.k), dtype=torch.int64, device="cuda")
         freed = [None, None]
         for i in range(n_chunks):
             b = i * chunk
@@ -615,8 +616,8 @@ class ScorePlan:
     def merge(self, d_lists, n_lists: int, out=None, stream=None):
         """K3 over [n_lists, n_seg, k] device tables -> [n_seg, k]."""
         torch = _torch()
-        out = out if out is not None else torch.zeros((self.n_seg, self.k), dtype=torch.int64,
-                                                       device="cuda")
+        out = out if out is not None else torch.empty((self.n_seg, self.k), dtype=torch.int64,
+                                                      device="cuda")
         _lib.check(_lib.load().occx_topk_merge(
             _lib.ctx(), _lib.ptr(d_lists), n_lists, self.n_seg, self.k, _lib.ptr(out),
             _lib.stream_ptr(stream)), "occx_topk_merge")

@@ -126,7 +126,10 @@ __global__ void __launch_bounds__(kMixThreads) mix_reduce_kernel(const __grid_co
     uint32_t nxt[kMixPer];
     for (uint32_t rb = 0; rb < len; rb += 32 * kMixPer) {
       const uint32_t nb = rb + 32 * kMixPer;
-      if (nb < len) {                                      // next chunk of this kernel
+      if (nb + 32 * kMixPer <= len) {                      // next chunk, fully inside
+#pragma unroll
+        for (int u = 0; u < kMixPer; ++u) nxt[u] = __ldcs(src + nb + (uint32_t)u * 32 + lane);
+      } else if (nb < len) {                               // next chunk, partial
 #pragma unroll
         for (int u = 0; u < kMixPer; ++u) {
           const uint32_t i = nb + (uint32_t)u * 32 + lane;

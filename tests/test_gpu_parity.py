@@ -374,3 +374,49 @@ def test_k2i_many_segments_and_score_space(P, torch):
     # the public API on the same space
     res = P.score_space(cfg.kernels[:3], cfg.archs, k=8)
     assert [e.key for e in res[0].entries] == [int(x) for x in want[0] if x]
+
+
+# ---------------------------------------------------------------------------
+# multi-process sharding with real GPU kernels (gloo transport; NCCL on 2-8 GPUs)
+# ---------------------------------------------------------------------------
+
+def _gpu_shard_worker(rank, world, port, name, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1701_08547_b200 as P
+    from paper_1701_08547_b200 import workloads
+    from paper_1701_08547_b200.dist import allgather_merge, shard_range
+    cfg = workloads.CONFIGS[name]()
+    plan = P.ScorePlan(cfg.kernels, cfg.archs, k=cfg.k)
+    b, e = shard_range(plan.total, rank, world)
+    rec = plan.generate(b, e - b)
+    local = plan.score(rec, e - b, index_base=b).cpu()          # K2 on this rank's shard
+    merged = allgather_merge(local, lambda g: plan.merge(g.cuda(), g.shape[0]).cpu())
+    if rank == 0:
+        q.put(merged.numpy().view(np.uint64).tolist())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_gpu_kernels_equal_golden(P, golden, world):
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_gpu_shard_worker, args=(r, world, port, "config4", q))
+          for r in range(world)]
+    for p_ in ps:
+        p_.start()
+    res = q.get(timeout=600)
+    for p_ in ps:
+        p_.join(timeout=120)
+        assert p_.exitcode == 0
+    assert res == golden("topk_config4.json")["corrected"]
