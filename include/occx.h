@@ -45,7 +45,10 @@ typedef enum occx_status {
   OCCX_ERR_NCCL = 7,
   OCCX_ERR_CAPACITY = 8,           /* input exceeds a documented table limit  */
   OCCX_ERR_KEY = 9,                /* KeyError (missing throughput entry)      */
-  OCCX_ERR_INDEX = 10              /* IndexError (empty thread-candidate list) */
+  OCCX_ERR_INDEX = 10,             /* IndexError (empty thread-candidate list) */
+  OCCX_ERR_PARSE = 11,             /* ParseError           errors.py:8-15     */
+  OCCX_ERR_EMPTY = 12,             /* EmptyInputError      errors.py:18       */
+  OCCX_ERR_ATTRIBUTE = 13          /* AttributeError: reference parser quirk, sass.py:278-279 */
 } occx_status;
 
 typedef enum occx_mode { OCCX_MODE_CORRECTED = 0, OCCX_MODE_VERBATIM = 1 } occx_mode;
@@ -261,6 +264,28 @@ int occx_score_space(const occx_ctx* ctx, const occx_arch_t* h_archs, int n_arch
 int occx_gen_space(const occx_ctx* ctx, const occx_segdesc_t* d_desc,
                    uint32_t n_desc, const uint32_t* d_pool, uint64_t begin,
                    uint64_t n, occx_cand_t* d_out, void* stream);
+
+/* ---- host: disassembly tokenizer -----------------
+ * Replaces parse_disassembly() sass.py:300-339 (+ parse_instruction_line
+ * :236-288, register_operand_count :105-107) for the K0 path: UTF-8 text
+ * (str encoded with 'surrogatepass') -> per-function names, CSR offsets and
+ * 4-byte OCCX_INSTR records over an interned signature table (opcode and
+ * modifiers joined by 0x1F, dots dropped).  Same functions, instructions and
+ * errors as the reference; on OCCX_ERR_PARSE / _ATTRIBUTE, *err_line is the
+ * 1-based line and occx_sass_error_text() the message (for the ';' error:
+ * the offending opcode token).  The result is owned by the library until
+ * occx_sass_free (also call it after errors).                           */
+typedef struct occx_sass occx_sass;
+int occx_sass_parse(const char* utf8, uint64_t n_bytes, occx_sass** out, int64_t* err_line);
+uint32_t occx_sass_n_kernels(const occx_sass* r);
+uint64_t occx_sass_n_instr(const occx_sass* r);
+const uint32_t* occx_sass_records(const occx_sass* r);
+const uint64_t* occx_sass_offsets(const occx_sass* r);
+const char* occx_sass_kernel_name(const occx_sass* r, uint32_t k);
+uint32_t occx_sass_n_sigs(const occx_sass* r);
+const char* occx_sass_signature(const occx_sass* r, uint32_t i);
+const char* occx_sass_error_text(const occx_sass* r);
+void occx_sass_free(occx_sass* r);
 
 #ifdef __cplusplus
 }

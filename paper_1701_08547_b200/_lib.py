@@ -67,6 +67,16 @@ SIGNATURES = {
                          _P, _P], _I),
     "occx_topk_merge": ([_P, _P, _U32, _U32, _U32, _P, _P], _I),
     "occx_gen_space": ([_P, _P, _U32, _P, _U64, _U64, _P, _P], _I),
+    "occx_sass_parse": ([ctypes.c_char_p, _U64, _P, _P], _I),
+    "occx_sass_n_kernels": ([_P], _U32),
+    "occx_sass_n_instr": ([_P], _U64),
+    "occx_sass_records": ([_P], _P),
+    "occx_sass_offsets": ([_P], _P),
+    "occx_sass_kernel_name": ([_P, _U32], ctypes.c_char_p),
+    "occx_sass_n_sigs": ([_P], _U32),
+    "occx_sass_signature": ([_P, _U32], ctypes.c_char_p),
+    "occx_sass_error_text": ([_P], ctypes.c_char_p),
+    "occx_sass_free": ([_P], None),
     "occx_score_space": ([_P, _P, _I, _P, _U32, _P, _U32, _U64, _U64, _I, _P, _U32, _U32, _U32,
                           _P, _U64, _P, _P], _I),
 }
@@ -75,7 +85,9 @@ SIGNATURES = {
 def header_functions(path: str = HEADER_PATH) -> list[str]:
     """Function names declared in include/occx.h."""
     text = open(path, encoding="utf-8").read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(occx_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(
+        r"^\s*(?:int|void|uint32_t|uint64_t|const char\*|const uint32_t\*|const uint64_t\*)"
+        r"\s+(occx_\w+)\s*\(", text, re.M)))
 
 
 _lib = None

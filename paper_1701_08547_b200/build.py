@@ -20,6 +20,8 @@ NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
           "-cudart", "shared"]
+CXX = os.environ.get("CXX", "g++")
+CXX_SOURCES = {"occx_sass.cpp": []}     # host-only C++ (tokenizer)
 SOURCES = {
     "occx_capi.cu": [],
     "occx_score.cu": [],
@@ -51,6 +53,17 @@ def build(verbose: bool = False) -> str:
                 sys.stderr.write(r.stdout + r.stderr)
             if r.returncode:
                 raise RuntimeError(f"nvcc failed on {src}")
+    for src, extra in CXX_SOURCES.items():
+        path = os.path.join(CSRC, src)
+        obj = os.path.join(BUILD, src.replace(".cpp", ".o"))
+        objs.append(obj)
+        if _stale(obj, [path] + header_deps):
+            cmd = [CXX, "-O3", "-std=c++17", "-fPIC", "-Wall", "-c", path, "-o", obj, *extra]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if verbose or r.returncode:
+                sys.stderr.write(r.stdout + r.stderr)
+            if r.returncode:
+                raise RuntimeError(f"c++ failed on {src}")
     if _stale(OUT, objs):
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", OUT, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)

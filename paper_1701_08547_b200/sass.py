@@ -1,0 +1,86 @@
+"""Native disassembly tokenizer -> K0 instruction records.
+
+``tokenize(text)`` runs ``occx_sass_parse`` (host C++ in liboccx.so, a
+restatement of occmix/sass.py:216-339) and returns per-function names, CSR
+offsets, 4-byte OCCX_INSTR records and the interned signature table; errors
+are raised as the reference raises them (``ParseError`` with the same line
+and message, ``EmptyInputError``, and ``AttributeError`` where the reference
+trips over its own opcode regex).  ``aggregate_text(text)`` feeds the records
+to the K0 reducer on the GPU: the equivalent of
+``[(name, aggregate(instrs)) for name, instrs in parse_disassembly(text)]``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import EmptyInputError, ParseError
+from .mix import DEFAULT_OPCLASSES, DEVICE_ID, OpClass, classify_signature
+
+
+@dataclass
+class SassRecords:
+    names: list            # function names, in file order (duplicates kept)
+    offsets: np.ndarray    # u64 [n + 1]
+    records: np.ndarray    # u32 OCCX_INSTR records
+    signatures: list       # (opcode, modifiers) per signature id
+
+    def class_lut(self, table=DEFAULT_OPCLASSES) -> np.ndarray:
+        """classify() of every signature (mix.py:176-187) as device class ids."""
+        lut = [DEVICE_ID[classify_signature(op, mods, table)] for op, mods in self.signatures]
+        return np.asarray(lut or [DEVICE_ID[OpClass.UNCLASSIFIED]], np.uint8)
+
+
+def tokenize(text: str) -> SassRecords:
+    lib = _lib.load()
+    data = text.encode("utf-8", "surrogatepass")
+    h = ctypes.c_void_p()
+    line = ctypes.c_int64(0)
+    st = lib.occx_sass_parse(data, len(data), ctypes.byref(h), ctypes.byref(line))
+    try:
+        if st:
+            err = lib.occx_sass_error_text(h).decode("utf-8", "surrogatepass")
+            if st == 12:
+                raise EmptyInputError(err)
+            if st == 11:
+                if err.startswith("\x01"):
+                    err = f"instruction {err[1:]!r} missing terminating ';'"
+                raise ParseError(err, int(line.value))
+            if st == 13:
+                raise AttributeError(err)
+            _lib.check(st, f"occx_sass_parse (line {line.value}): {err}")
+        n_k = lib.occx_sass_n_kernels(h)
+        n_i = lib.occx_sass_n_instr(h)
+        names = [lib.occx_sass_kernel_name(h, k).decode("utf-8", "surrogatepass")
+                 for k in range(n_k)]
+        off = np.ctypeslib.as_array(ctypes.cast(lib.occx_sass_offsets(h),
+                                                ctypes.POINTER(ctypes.c_uint64)),
+                                    shape=(n_k + 1,)).copy() if n_k else np.zeros(1, np.uint64)
+        rec = np.ctypeslib.as_array(ctypes.cast(lib.occx_sass_records(h),
+                                                ctypes.POINTER(ctypes.c_uint32)),
+                                    shape=(n_i,)).copy() if n_i else np.zeros(0, np.uint32)
+        sigs = []
+        for i in range(lib.occx_sass_n_sigs(h)):
+            parts = lib.occx_sass_signature(h, i).decode("utf-8", "surrogatepass").split("\x1f")
+            sigs.append((parts[0], tuple("." + m for m in parts[1:])))
+        return SassRecords(names, off, rec, sigs)
+    finally:
+        lib.occx_sass_free(h)
+
+
+def aggregate_text(text: str, table=DEFAULT_OPCLASSES) -> list:
+    """[(name, InstructionMix)] for every function of a listing: native
+    tokenizer + K0 on the GPU."""
+    from .batch import _to_device, _to_host, mix_from_record, mix_reduce
+    r = tokenize(text)
+    if not r.names:
+        return []
+    lut = r.class_lut(table)
+    d = mix_reduce(_to_device(r.records if len(r.records) else np.zeros(1, np.uint32)),
+                   _to_device(r.offsets), len(r.names), _to_device(lut), len(lut))
+    out = _to_host(d, _lib.MIX, len(r.names))
+    return [(n, mix_from_record(m)) for n, m in zip(r.names, out)]

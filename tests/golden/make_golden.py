@@ -306,6 +306,114 @@ def topk_golden(name):
         json.dump(res, fh)
 
 
+# ---------------------------------------------------------------------------
+# disassembly tokenizer: reference parse_disassembly over fuzzed listings
+# ---------------------------------------------------------------------------
+
+_WS = [" ", "\t", "  ", "\xa0", "\u2003", "\x1f", "\u3000"]
+_NL = ["\n", "\r\n", "\r", "\x0b", "\x0c", "\x1c", "\x85", "\u2028"]
+
+
+def _rand_instr_line(rng):
+    ops = list(W.corpus_opcodes()) + ["FFMA", "LDG", "BRA", "EXIT", "lower", "F2F", "X1", "Q"]
+    op = rng.choice(ops)
+    mods = "".join(rng.choice([".E", ".F64", ".S64", ".GE", ".AND", ".X", ".", "..", ".\u00e9", ".7"])
+                   for _ in range(rng.randrange(0, 3)))
+    opnds = [rng.choice(["R1", "R22", "RZ", "R٣", "R3x", "xR4", "-R5", "|R6|", "[R7+0x8]", "R8.64",
+                         "[R9+R10]", "c[0x0][0x44]", "P0", "PT", "0x10", "SR_TID.X", "R²", "Rⅷ",
+                         "R1\u00e9", "éR2", "R0_", " "]) for _ in range(rng.randrange(0, 5))]
+    sep = rng.choice([", ", ",", " , ", ",,", ",\t"])
+    body = op + mods + ((rng.choice([" ", " ", "\t", "  "]) + sep.join(opnds)) if opnds else "")
+    pred = rng.choice(["", "", "", "@P0 ", "@!P1 ", "@PT ", "@!PT ", "@P ", "@Pé ", "@!P "])
+    semi = rng.choice([" ;", ";", " ;", "", " ;;", "; ", " ; /* 0x0012 */"])
+    addr = rng.choice(["", "/*0008*/ ", "  /* 0a8f */  ", "/*xyz*/ ", "/* 12 */"])
+    ctrl = rng.choice(["", "", "[B------:R-:W-:-:S04] ", "[-:x] ", "[] "])
+    wrap = rng.choice(["{}", "", "", "{", "}"])
+    line = ctrl + addr + pred + body + semi
+    if wrap == "{}":
+        line = "{ " + line + " }"
+    elif wrap:
+        line = wrap + line
+    tail = rng.choice(["", "", " /* 0x00 */", " /* a */ /* b */", " */", " /*", "  "])
+    return rng.choice(_WS[:3]) + line + tail
+
+
+def _rand_other_line(rng):
+    return rng.choice([
+        "Function : k" + str(rng.randrange(5)), "  Function:  k" + str(rng.randrange(5)) + "  ",
+        "Function : a b", "\t.section\t.text.kern" + str(rng.randrange(3)) + ",\"ax\",@progbits",
+        ".section  .text.", "L" + str(rng.randrange(3)) + ":", "  $x.y@z :  ", ".L_24:", "BB0_1 :",
+        "// comment", "/* only a comment */", ".headerflags @\"EF\"", "", "   ", "{", "}",
+        "9abc:", "lbl: x", "Function", "@P0", "@P0  ", "  /*0010*/  ", "\u00e9t\u00e9:",
+    ])
+
+
+def _rand_listing(rng):
+    lines = []
+    for _ in range(rng.randrange(1, 40)):
+        lines.append(_rand_instr_line(rng) if rng.random() < 0.7 else _rand_other_line(rng))
+    if rng.random() < 0.8:
+        lines.insert(rng.randrange(0, max(1, len(lines) // 3)), rng.choice(
+            ["Function : kern", "\t.section\t.text.kern,\"ax\"", "kern:"]))
+    text = ""
+    for ln in lines:
+        text += ln + rng.choice(_NL[:1] * 6 + _NL)
+    return text if rng.random() < 0.9 else text.rstrip("\n")
+
+
+def _ref_summary(text):
+    try:
+        funcs = R.parse_disassembly(text)
+    except R.StaticAnalysisError as exc:
+        return ["err", type(exc).__name__, getattr(exc, "line", None), str(exc)]
+    except Exception as exc:  # reference quirks (e.g. AttributeError)
+        return ["err", type(exc).__name__, None, str(exc)]
+    return ["ok", [[name, [[i.opcode, list(i.modifiers), i.predicate is not None,
+                            i.register_operand_count] for i in instrs]] for name, instrs in funcs]]
+
+
+def sass_golden(n=4000):
+    rng = random.Random(0x5A55)
+    cases = []
+    corpus = W.corpus_text(W.make_corpus(40)).splitlines()
+    for i in range(n):
+        kind = i % 5
+        if kind in (0, 1):
+            text = _rand_listing(rng)
+        elif kind == 2:                                   # mutated corpus listing
+            a = rng.randrange(0, len(corpus) - 60)
+            lines = corpus[a:a + rng.randrange(1, 60)]
+            if rng.random() < 0.7:
+                lines.insert(0, "\tFunction : k")
+            for _ in range(rng.randrange(0, 4)):
+                j = rng.randrange(len(lines))
+                lines[j] = rng.choice([_rand_instr_line(rng), _rand_other_line(rng),
+                                       lines[j].replace(";", ""), lines[j].replace(" ", "\t", 1),
+                                       lines[j] + " /* 0xff */", "@!P2 " + lines[j].strip()])
+            text = rng.choice(_NL[:2]).join(lines)
+        elif kind == 3:                                   # acceptance-style printable fuzz
+            printable = ("ABCDEFGHIJKLMNOPQRSTUVWXYZ0123456789 \t;:,.[]@/*-_'\"()\n"
+                         "abcdefghijklmnopqrstuvwxyz{}!#=")
+            text = "".join(rng.choice(printable) for _ in range(rng.randrange(0, 160)))
+        else:                                             # latin-1 bytes / wide code points
+            if rng.random() < 0.5:
+                text = bytes(rng.randrange(256) for _ in range(rng.randrange(0, 120))).decode("latin-1")
+            else:
+                text = "".join(chr(rng.choice([rng.randrange(32, 127), rng.randrange(0x80, 0x3000),
+                                               0x2028, 0x0663, 0x00b2, 0x2167, 0xd800]))
+                               for _ in range(rng.randrange(0, 80)))
+                text = "Function : k\n" + text
+        cases.append({"text": text, "result": _ref_summary(text)})
+    kinds = {}
+    for c in cases:
+        key = c["result"][0] if c["result"][0] == "ok" else c["result"][1]
+        kinds[key] = kinds.get(key, 0) + 1
+    with open(os.path.join(HERE, "sass_fuzz.json"), "w") as fh:
+        json.dump({"meta": META, "outcomes": kinds, "cases": cases}, fh,
+                  ensure_ascii=True)
+    print("sass outcomes", kinds)
+
+
 if __name__ == "__main__":
     steps = sys.argv[1:] or ["tables", "random", "suggest", "mix", "corpus", "config1",
                              "config2", "config4"]
@@ -314,5 +422,6 @@ if __name__ == "__main__":
     for s in steps:
         t0 = time.time()
         {"tables": occupancy_tables, "random": occupancy_random, "suggest": suggest_golden,
-         "mix": mix_golden, "corpus": corpus_golden}.get(s, lambda: topk_golden(s))()
+         "mix": mix_golden, "corpus": corpus_golden, "sass": sass_golden}.get(
+            s, lambda: topk_golden(s))()
         print(f"{s}: {time.time() - t0:.1f}s", flush=True)

@@ -420,3 +420,16 @@ def test_sharded_gpu_kernels_equal_golden(P, golden, world):
         p_.join(timeout=120)
         assert p_.exitcode == 0
     assert res == golden("topk_config4.json")["corrected"]
+
+
+def test_tokenizer_plus_k0_corpus_golden(P, torch, golden):
+    """Listing text -> native tokenizer -> K0 on the GPU == reference
+    parse_disassembly + aggregate (names, counts in insertion order, regs)."""
+    from paper_1701_08547_b200 import sass, workloads
+    g = golden("corpus.json")
+    res = sass.aggregate_text(workloads.corpus_text(workloads.make_corpus(g["n_kernels"])))
+    assert len(res) == len(g["kernels"])
+    for (name, mx), (gname, pairs, reg) in zip(res, g["kernels"]):
+        assert name == gname
+        assert [[c.value, n] for c, n in mx.counts.items()] == pairs
+        assert mx.reg_operands == reg
