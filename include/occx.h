@@ -93,10 +93,12 @@ typedef struct occx_occ_t {
   double occupancy;
 } occx_occ_t;
 
-/* Instruction record for the mix reducer: bits 0-15 signature id, 16-23
- * register-operand count (sass.py:105-107), bit 24 predicate guard.       */
+/* Instruction record for the mix reducer: bit 0 predicate guard, bits 1-16
+ * signature id, bits 17-24 register-operand count (sass.py:105-107), bits
+ * 25-31 zero.  The low 17 bits (sig << 1 | guard) index the reducer's
+ * class table directly.                                                   */
 #define OCCX_INSTR(sig, regops, guard) \
-  ((uint32_t)(sig) | ((uint32_t)(regops) << 16) | ((uint32_t)(guard) << 24))
+  ((uint32_t)(guard) | ((uint32_t)(sig) << 1) | ((uint32_t)(regops) << 17))
 
 /* InstructionMix (mix.py:194-208) in device form.  144 B.
  * counts[c] for device class c (14 OpClass rows in enum order, then

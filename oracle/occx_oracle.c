@@ -212,7 +212,7 @@ void ora_topk_merge(const uint64_t* lists, int64_t n_lists, int64_t n_seg, int64
 
 /* ------------------------------------------------------------------------
  * aggregate() mix.py:245-261 over 4-byte instruction records
- * (sig:16 | regops:8 | guard:1).  class ids: 0..13 OpClass rows in enum
+ * (guard:1 | sig:16 | regops:8, include/occx.h OCCX_INSTR).  class ids: 0..13 OpClass rows in enum
  * order, 14 = Unclassified; CTRL rows are 11..13 (Pred, Ctrl, Move).
  * order_out[k][j] = class of the j-th dict insertion (-1 = none).
  * --------------------------------------------------------------------- */
@@ -229,17 +229,17 @@ void ora_aggregate(const uint32_t* rec, const uint64_t* off, int64_t n_kernels,
     int64_t regs = 0;
     for (uint64_t i = off[kk]; i < off[kk + 1]; ++i) {
       uint32_t r = rec[i];
-      uint32_t sig = r & 0xffffu;
+      uint32_t sig = (r >> 1) & 0xffffu;
       int cls = sig < (uint64_t)n_sig ? sig_class[sig] : 14;
       if (!present[cls]) { present[cls] = 1; order[n_order++] = cls; }
       counts[cls] += 1;
-      int guard = (r >> 24) & 1;
+      int guard = r & 1;
       int is_ctrl = cls >= 11 && cls <= 13;
       if (guard && !is_ctrl) {
         if (!present[11]) { present[11] = 1; order[n_order++] = 11; }
         counts[11] += 1;
       }
-      regs += (r >> 16) & 0xffu;
+      regs += (r >> 17) & 0xffu;
     }
     regops_out[kk] = regs;
   }

@@ -239,7 +239,7 @@ def pack_instructions(kernels, sigs: SignatureTable):
             nreg = register_operand_count(ins)
             if nreg > 255:
                 raise DeviceError("instruction with more than 255 register operands")
-            recs.append(sid | (nreg << 16) | ((1 if ins.predicate else 0) << 24))
+            recs.append((1 if ins.predicate else 0) | (sid << 1) | (nreg << 17))   # OCCX_INSTR
         offs.append(len(recs))
     return np.asarray(recs, np.uint32), np.asarray(offs, np.uint64)
 

@@ -81,13 +81,19 @@ __global__ void __launch_bounds__(kMixThreads) mix_reduce_kernel(const __grid_co
     inc[i] = v;
   }
   for (uint32_t i = threadIdx.x; i < (kMixThreads / 32) * 17; i += blockDim.x) firsts[i] = kAbsent;
-  for (uint32_t i = threadIdx.x; i <= p.n_sig; i += blockDim.x)
-    lut[i] = i < p.n_sig ? (uint8_t)(p.sig_class[i] & 15u) : (uint8_t)kNullClass;
+  // class table indexed by the record's low 17 bits (sig << 1 | guard):
+  // entry = class | 16 when the guard adds a PredIns (class not CTRL);
+  // signature n_sig is the padding record (class 15, counts nothing)
+  for (uint32_t i = threadIdx.x; i <= p.n_sig; i += blockDim.x) {
+    const uint32_t c = i < p.n_sig ? (p.sig_class[i] & 15u) : kNullClass;
+    lut[2 * i] = (uint8_t)c;
+    lut[2 * i + 1] = (uint8_t)(c | ((c < 11 || c == 14) ? 16u : 0u));
+  }
   __syncthreads();
   const uint32_t inc_base = (uint32_t)__cvta_generic_to_shared(inc);
   const uint32_t lut_base = (uint32_t)__cvta_generic_to_shared(lut);
   uint32_t* my_first = firsts + (threadIdx.x >> 5) * 17;
-  const uint32_t null_rec = p.n_sig;                        // sig = n_sig -> class 15
+  const uint32_t null_rec = p.n_sig << 1;                   // sig = n_sig -> class 15
 
   const int lane = threadIdx.x & 31;
   const uint32_t warps_total = gridDim.x * (kMixThreads / 32);
@@ -146,13 +152,12 @@ __global__ void __launch_bounds__(kMixThreads) mix_reduce_kernel(const __grid_co
 #pragma unroll
       for (int u = 0; u < kMixPer; ++u) {
         const uint32_t r = rec[u];
-        const uint32_t c = lds_u8(lut_base + (r & 0xffffu));
-        const uint32_t idx = c | ((r >> 20) & 16u);         // guard bit 24 -> bit 4
+        const uint32_t idx = lds_u8(lut_base + (r & 0x1ffffu));  // class | counted-guard << 4
         uint32_t d0, d1;
         asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(d0), "=r"(d1) : "r"(inc_base + idx * 8u));
         v0 += d0;
         v1 += d1;
-        regs += __byte_perm(r, 0, 0x4442);                  // register operands (byte 2)
+        regs += r >> 17;                                    // register operands (bits 17-24)
       }
       // classes (nibbles) present in this lane's chunk -> warp presence
       uint32_t t0 = v0 | (v0 >> 1), t1 = v1 | (v1 >> 1);
@@ -165,12 +170,13 @@ __global__ void __launch_bounds__(kMixThreads) mix_reduce_kernel(const __grid_co
         seen_hi |= pres_hi;
 #pragma unroll
         for (int u = 0; u < kMixPer; ++u) {                // rare: re-read the classes
-          const uint32_t c = lds_u8(lut_base + (rec[u] & 0xffffu));
+          const uint32_t idx = lds_u8(lut_base + (rec[u] & 0x1ffffu));
+          const uint32_t c = idx & 15u;
           const uint32_t pos = rb + (uint32_t)u * 32 + lane;
           if (c != kNullClass) {
             atomicMin(my_first + c, 2u * pos);
             // guard PredIns (non-CTRL class): key 2*pos + 1, tracked in slot 16
-            if (((rec[u] >> 24) & 1u) && !(c >= 11 && c <= 13)) atomicMin(my_first + 16, 2u * pos + 1);
+            if (idx & 16u) atomicMin(my_first + 16, 2u * pos + 1);
           }
         }
       }
@@ -236,7 +242,7 @@ extern "C" int occx_mix_reduce(const occx_ctx* ctx, const uint32_t* d_instr,
   p.sig_class = d_sig_class;
   p.n_sig = n_sig;
   p.out = d_out;
-  const size_t smem = 32 * 8 + ((kMixThreads / 32) * 17 + 2) * 4 + ((n_sig + 1 + 15) & ~15u);
+  const size_t smem = 32 * 8 + ((kMixThreads / 32) * 17 + 2) * 4 + ((2 * (n_sig + 1) + 15) & ~15u);
   if (smem > 48 * 1024 &&
       cudaFuncSetAttribute(mix_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)

@@ -11,9 +11,9 @@
 //   * an opcode followed by a non-space separator (tab) or a second ';'
 //     makes the reference raise AttributeError (sass.py:278-279 matches the
 //     opcode regex on `body.partition(" ")[0]`): status OCCX_ERR_ATTRIBUTE.
-// Record = signature id (interned opcode + modifiers) | register operands
-// (`\bR\d+\b` matches over the operand tokens, sass.py:57,84-88,105-107)
-// << 16 | predicate guard << 24.
+// Record = OCCX_INSTR(signature id (interned opcode + modifiers), register
+// operands (`\bR\d+\b` matches over the operand tokens,
+// sass.py:57,84-88,105-107), predicate guard).
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -476,7 +476,7 @@ void parse_chunk(const unsigned char* s, size_t n, Chunk& ck) {
     } else {
       id = it->second;
     }
-    ck.recs.push_back(id | (pi.regops << 16) | ((pi.guard ? 1u : 0u) << 24));
+    ck.recs.push_back(OCCX_INSTR(id, pi.regops, pi.guard ? 1u : 0u));
   }
 }
 
@@ -574,7 +574,7 @@ extern "C" int occx_sass_parse(const char* text, uint64_t n_bytes, occx_sass** o
       }
       if (j < c.recs.size()) {
         const uint32_t x = c.recs[j];
-        r->records.push_back(remap[x & 0xffffu] | (x & 0xffff0000u));
+        r->records.push_back((remap[(x >> 1) & 0xffffu] << 1) | (x & 0xfffe0001u));
       }
     }
     if (c.err) {

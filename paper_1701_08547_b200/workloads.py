@@ -233,7 +233,7 @@ def corpus_records(c: Corpus) -> np.ndarray:
     sig = c.opcode.astype(np.uint32) * np.uint32(len(MOD_SUBSETS)) + c.subset.astype(np.uint32)
     regops = _REGS_OF_TEMPLATE[c.ops].sum(axis=1).astype(np.uint32)
     guard = (c.guard > 0).astype(np.uint32)
-    return sig | (regops << np.uint32(16)) | (guard << np.uint32(24))
+    return guard | (sig << np.uint32(1)) | (regops << np.uint32(17))
 
 
 def corpus_text(c: Corpus, kernels=None) -> str:

@@ -166,6 +166,6 @@ def test_corpus_deterministic_and_sliceable():
     b = workloads.make_corpus(20, first=30)
     ra, rb = workloads.corpus_records(a), workloads.corpus_records(b)
     assert np.array_equal(ra[int(a.offsets[30]):], rb)
-    assert (ra >> 25).max() == 0 and ((ra >> 16) & 0xFF).max() <= 4
+    assert (ra >> 25).max() == 0 and ((ra >> 17) & 0xFF).max() <= 4
     lengths = np.diff(a.offsets.astype(np.int64))
     assert lengths.min() >= 32 and lengths.max() <= 32 + 1984

@@ -21,8 +21,8 @@ def _summary(text):
     for k, name in enumerate(r.names):
         instrs = []
         for rec in r.records[int(r.offsets[k]):int(r.offsets[k + 1])]:
-            op, mods = r.signatures[int(rec) & 0xFFFF]
-            instrs.append([op, list(mods), bool((int(rec) >> 24) & 1), (int(rec) >> 16) & 0xFF])
+            op, mods = r.signatures[(int(rec) >> 1) & 0xFFFF]
+            instrs.append([op, list(mods), bool(int(rec) & 1), (int(rec) >> 17) & 0xFF])
         out.append([name, instrs])
     return ["ok", out]
 
@@ -50,9 +50,10 @@ def test_corpus_text_matches_generator_records():
     np.testing.assert_array_equal(r.offsets, c.offsets)
     ops = workloads.corpus_opcodes()
     want_sig = [(ops[o], workloads.MOD_SUBSETS[s]) for o, s in zip(c.opcode, c.subset)]
-    assert [r.signatures[x & 0xFFFF] for x in r.records] == want_sig
+    assert [r.signatures[(x >> 1) & 0xFFFF] for x in r.records] == want_sig
     rec = workloads.corpus_records(c)
-    np.testing.assert_array_equal(r.records >> 16, rec >> 16)       # regops + guard
+    np.testing.assert_array_equal(r.records >> 17, rec >> 17)       # regops
+    np.testing.assert_array_equal(r.records & 1, rec & 1)           # guard
 
 
 def test_corpus_aggregate_golden_via_tokenizer():
