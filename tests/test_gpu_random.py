@@ -157,3 +157,61 @@ def test_random_mixes_features_vs_pyref():
                 assert [x.hex() for x in got.shares.values()] == \
                     [x.hex() for x in pyref.pipeline_utilization(counts, mix.reg_operands,
                                                                  cc).values()]
+
+
+def _k0_run(rec_dev, off, lut):
+    import torch
+    from paper_1701_08547_b200 import _lib, batch
+    n = len(off) - 1
+    d = batch.mix_reduce(rec_dev, batch._to_device(off), n, batch._to_device(lut), len(lut))
+    torch.cuda.synchronize()
+    return batch._to_host(d, _lib.MIX, n)
+
+
+def _k0_check(out, rec, off, lut):
+    counts, order, regs = oracle.aggregate_records(rec, off, lut)
+    np.testing.assert_array_equal(out["counts"][:, :15].astype(np.int64), counts)
+    np.testing.assert_array_equal(out["reg_operands"].astype(np.int64), regs)
+    np.testing.assert_array_equal(out["n_instr"].astype(np.int64), np.diff(off.astype(np.int64)))
+    fk = np.where(out["counts"][:, :15] > 0, out["first_key"][:, :15].astype(np.int64), 1 << 40)
+    got = np.argsort(fk, axis=1, kind="stable")
+    mask = np.arange(15)[None, :] < (counts > 0).sum(1)[:, None]
+    np.testing.assert_array_equal(np.where(mask, got, -1), order)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_k0_ragged_segments_vs_oracle(seed):
+    """K0 on ragged CSR layouts: empty kernels (leading, interior, trailing),
+    1-record kernels, kernels longer than a warp's record share, a nonzero
+    first offset, and record buffers at every 4-byte misalignment (the
+    vector path needs 16-byte alignment; the scalar path covers the rest)."""
+    import torch
+    from paper_1701_08547_b200 import batch
+    rng = np.random.default_rng(1000 + seed)
+    n_sig = int(rng.integers(1, 3000))
+    lut = rng.integers(0, 15, n_sig).astype(np.uint8)
+    kind = seed % 3
+    n_k = int(rng.integers(1, 5000))
+    if kind == 0:       # mostly tiny, many empty
+        lens = rng.integers(0, 40, n_k) * (rng.random(n_k) > 0.3)
+    elif kind == 1:     # a few huge kernels among normal ones
+        lens = rng.integers(32, 2048, n_k)
+        lens[rng.integers(0, n_k, 3)] = rng.integers(200_000, 2_000_000, 3)
+    else:               # empties at both ends
+        lens = rng.integers(1, 3000, n_k)
+        lens[:5] = 0
+        lens[-7:] = 0
+    n_rec = int(lens.sum())
+    lead = int(rng.integers(0, 9))          # records before the first kernel
+    sig = rng.integers(0, n_sig, n_rec + lead).astype(np.uint32)
+    regops = rng.integers(0, 256, n_rec + lead).astype(np.uint32)
+    guard = (rng.random(n_rec + lead) < 0.15).astype(np.uint32)
+    rec = guard | (sig << 1) | (regops << 17)
+    off = (lead + np.concatenate([[0], np.cumsum(lens)])).astype(np.uint64)
+    for mis in (0, 1, 2, 3):
+        buf = np.zeros(len(rec) + 4, np.uint32)
+        buf[mis:mis + len(rec)] = rec
+        d = batch._to_device(buf)
+        view = d[4 * mis:]                 # byte view shifted by 4*mis bytes
+        out = _k0_run(view, off, lut)
+        _k0_check(out, rec, off, lut)
