@@ -150,9 +150,12 @@ def occupancy_batch(archs, launches, mode: Mode = Mode.CORRECTED, arch_index=Non
 # K4: suggest
 # ---------------------------------------------------------------------------
 
-def suggest_batch(requests, mode: Mode = Mode.CORRECTED) -> list[SuggestionReport]:
+def suggest_batch(requests, mode: Mode = Mode.CORRECTED,
+                  raise_first: bool = True) -> list[SuggestionReport]:
     """suggest(arch, resources, mode, dynamic_shared_mem) for many requests
-    (ref occupancy.py:232-279).  requests: (arch, resources[, dynamic])."""
+    (ref occupancy.py:232-279).  requests: (arch, resources[, dynamic]).
+    With ``raise_first=False`` a failing request yields the exception the
+    reference would raise, in place, instead of raising it."""
     mode = Mode(mode)
     archs: list[ArchSpec] = []
     index: dict[int, int] = {}
@@ -182,13 +185,29 @@ def suggest_batch(requests, mode: Mode = Mode.CORRECTED) -> list[SuggestionRepor
         arch, res = req[0], req[1]
         o = out[i]
         st = int(o["status"])
+        err = None
         if st == 2:
-            raise IllegalLaunchError(
-                f"{res.registers_per_thread} registers/thread or "
-                f"{int(inp[i]['smem'])} bytes of shared memory exceed {arch.name}")
-        if st == 10:
-            raise IndexError("tuple index out of range")
-        _lib.check(st, "occx_suggest_batch")
+            regs, smem = res.registers_per_thread, int(inp[i]["smem"])
+            if regs > arch.max_regs_per_thread:          # occupancy.py:245-248
+                err = IllegalLaunchError(
+                    f"{regs} registers/thread exceeds the {arch.max_regs_per_thread} "
+                    f"supported by {arch.name}")
+            else:                                        # occupancy.py:249-252
+                err = IllegalLaunchError(
+                    f"{smem} bytes of shared memory exceeds the "
+                    f"{arch.shared_mem_per_block}-byte block capacity of {arch.name}")
+        elif st == 10:
+            err = IndexError("tuple index out of range")
+        elif st:
+            try:
+                _lib.check(st, "occx_suggest_batch")
+            except Exception as exc:   # noqa: BLE001 -- mapped status
+                err = exc
+        if err is not None:
+            if raise_first:
+                raise err
+            reports.append(err)
+            continue
         reports.append(SuggestionReport(
             thread_candidates=thread_candidates(arch),
             registers_used=res.registers_per_thread,

@@ -259,3 +259,35 @@ def corpus_text(c: Corpus, kernels=None) -> str:
             addr = (i - int(c.offsets[k])) * 16
             lines.append(f"        /*{addr:04x}*/                   {body} ;")
     return "\n".join(lines) + "\n"
+
+
+def corpus_resource_report(n_kernels: int, seed: int, rmax: int, smax: int) -> str:
+    """Synthetic ptxas -v report for corpus kernels kern_000000..: every
+    7th name is absent from the listing (empty stream + warning), one name
+    repeats, clauses vary (smem, cmem banks, spills, lmem)."""
+    import random
+    rng = random.Random(seed)
+    lines = ["ptxas info    : 0 bytes gmem"]
+    names = [f"kern_{k:06d}" for k in range(n_kernels)]
+    names[::7] = [f"missing_{k}" for k in range(len(names[::7]))]
+    names.append(names[3])
+    for i, name in enumerate(names):
+        sm = rng.choice(("20", "35", "52", "60", "100a", None))
+        lines.append(f"ptxas info    : Compiling entry function '{name}'" +
+                     (f" for 'sm_{sm}'" if sm else ""))
+        if rng.random() < 0.2:
+            lines.append(f"ptxas info    : Function properties for {name}")
+            lines.append(f"    {rng.randrange(0, 64)} bytes stack frame, "
+                         f"{rng.randrange(0, 9)} bytes spill stores, "
+                         f"{rng.randrange(0, 9)} bytes spill loads")
+        clauses = [f"{rng.randrange(0, rmax + 1)} registers"]
+        if rng.random() < 0.6:
+            clauses.append(f"{rng.choice((0, 4, 1024, 3072, 6144, 12288, smax))} bytes smem")
+        if rng.random() < 0.8:
+            clauses.append(f"{rng.randrange(320, 400)} bytes cmem[0]")
+        if rng.random() < 0.2:
+            clauses.append(f"{rng.randrange(0, 64)} bytes cmem[2]")
+        if rng.random() < 0.1:
+            clauses.append("8 bytes lmem")
+        lines.append("ptxas info    : Used " + ", ".join(clauses))
+    return "\n".join(lines) + "\n"

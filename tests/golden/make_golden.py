@@ -414,6 +414,80 @@ def sass_golden(n=4000):
     print("sass outcomes", kinds)
 
 
+# ---------------------------------------------------------------------------
+# analysis reports (occmix analyze data path, ref cli.py:105-134)
+# ---------------------------------------------------------------------------
+
+def _ref_analyze(arch, mode, res_text, sass_text, space=None, scale=1.0, dyn=0):
+    """The body of cmd_analyze (ref cli.py:105-128) -> (json text | error)."""
+    try:
+        resources = R.parse_resource_report(res_text)
+        by_name = {n: ins for n, ins in R.parse_disassembly(sass_text)}
+        analyses = [R.analyze_kernel(arch, r, by_name.get(r.entry_name, []), mode,
+                                     dynamic_shared_mem=dyn,
+                                     space=space if space is not None else R.TuningSpace(),
+                                     scale=scale)
+                    for r in resources]
+        text = R.to_json(R.report_dict(arch, mode, analyses))
+        return {"ok": True, "sha256": hashlib.sha256(text.encode()).hexdigest(),
+                "kernels": [hashlib.sha256(json.dumps(R.report.kernel_dict(a), indent=2)
+                                           .encode()).hexdigest()[:16] for a in analyses],
+                "text": text if len(text) < 40000 else None}
+    except Exception as exc:   # noqa: BLE001
+        return {"ok": False, "error": type(exc).__name__, "message": str(exc)}
+
+
+REPORT_CASES = (   # (tag, arch index, mode, space spec, scale, dynamic smem)
+    ("default", None, "corrected", None, 1.0, 0),
+    ("verbatim", None, "verbatim", None, 1.0, 0),
+    ("space_scale_dyn", None, "corrected",
+     ((64, 128, 192, 256, 384, 512, 1024), (8, 16), (1, 2), (16, 48), ("", "-O3")), 2.5, 1024),
+)
+
+
+def report_golden(n_kernels=120):
+    atax_res = open("/root/reference/pkg/tests/data/atax_kepler.ptxas.txt").read()
+    atax_sass = open("/root/reference/pkg/tests/data/atax_kepler.sass.txt").read()
+    c = W.make_corpus(n_kernels)
+    sass = W.corpus_text(c)
+    out = {"meta": META, "n_kernels": n_kernels,
+           "sass_sha256": hashlib.sha256(sass.encode()).hexdigest(),
+           "atax": {"ptxas": atax_res, "sass": atax_sass, "runs": []}, "corpus": []}
+    for ai, A in enumerate(ARCHS):
+        for tag, _, mode, sp, scale, dyn in REPORT_CASES:
+            space = None if sp is None else R.TuningSpace(*sp)
+            m = R.Mode(mode)
+            out["atax"]["runs"].append({"arch": ai, "case": tag, "result":
+                                        _ref_analyze(A, m, atax_res, atax_sass, space, scale, dyn)})
+            res_text = W.corpus_resource_report(n_kernels, 1000 * ai + len(tag),
+                                               A.max_regs_per_thread, A.shared_mem_per_block - dyn)
+            r = _ref_analyze(A, m, res_text, sass, space, scale, dyn)
+            r["text"] = None
+            r["resources"] = [[x.entry_name, x.registers_per_thread, x.static_shared_mem,
+                               [list(b) for b in x.const_mem_banks], x.spill_loads,
+                               x.spill_stores, x.target_cc]
+                              for x in R.parse_resource_report(res_text)]
+            out["corpus"].append({"arch": ai, "case": tag, "seed": 1000 * ai + len(tag),
+                                  "result": r})
+    # error paths: registers / smem above the arch limit, scale <= 0, empty report
+    errs = []
+    k = R.builtin_arch("kepler")
+    for tag, res_text, scale in (
+            ("regs", "Compiling entry function 'kern_000001'\nptxas info : Used 300 registers\n", 1.0),
+            ("smem", "Compiling entry function 'kern_000001'\nptxas info : Used 8 registers, "
+                     "99999 bytes smem\n", 1.0),
+            ("scale", "Compiling entry function 'kern_000001'\nptxas info : Used 8 registers\n", 0.0),
+            ("empty", "ptxas info : 0 bytes gmem\n", 1.0),
+            ("clause", "Compiling entry function 'k'\nptxas info : Used many registers\n", 1.0)):
+        errs.append({"case": tag, "resources": res_text, "scale": scale,
+                     "result": _ref_analyze(k, R.Mode.CORRECTED, res_text, sass, None, scale)})
+    out["errors"] = errs
+    with open(os.path.join(HERE, "report.json"), "w") as fh:
+        json.dump(out, fh)
+    print("report cases", sum(r["result"]["ok"] for r in out["corpus"]), "ok of",
+          len(out["corpus"]))
+
+
 if __name__ == "__main__":
     steps = sys.argv[1:] or ["tables", "random", "suggest", "mix", "corpus", "config1",
                              "config2", "config4"]
@@ -422,6 +496,7 @@ if __name__ == "__main__":
     for s in steps:
         t0 = time.time()
         {"tables": occupancy_tables, "random": occupancy_random, "suggest": suggest_golden,
-         "mix": mix_golden, "corpus": corpus_golden, "sass": sass_golden}.get(
+         "mix": mix_golden, "corpus": corpus_golden, "sass": sass_golden,
+         "report": report_golden}.get(
             s, lambda: topk_golden(s))()
         print(f"{s}: {time.time() - t0:.1f}s", flush=True)
