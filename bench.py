@@ -264,6 +264,11 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=4_000_000)
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every GPU scores a full copy of the workload (default); "
+                         "strong: the GPUs split one copy")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: test harness for several ranks on one GPU")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -299,36 +304,60 @@ def main():
     import numpy as np
     import torch
     import torch.distributed as dist
-    torch.cuda.set_device(local)
+    gloo = args.dist_backend == "gloo"
+    # gloo harness: several ranks may share the box's only GPU
+    torch.cuda.set_device(local % torch.cuda.device_count() if gloo else local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if gloo:       # single-GPU test harness: ranks share a device, host-side collectives
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1701_08547_b200 import ScorePlan, workloads
-    from paper_1701_08547_b200.dist import allgather_merge, shard_range
+    from paper_1701_08547_b200.dist import allgather_merge, score_space_multi, shard_range
 
     cfg = workloads.CONFIGS[args.workload]()
     plan = ScorePlan(cfg.kernels, cfg.archs, args.mode, k=cfg.k)
-    begin, end = shard_range(plan.total, rank, world)
-    n = end - begin
+    if args.scaling == "weak":
+        # every rank scores its own copy of the space (global indices
+        # [rank*total, (rank+1)*total)); the whole job is world*total candidates
+        begin, n = 0, plan.total
+        key_base = rank * plan.total
+        global_total = world * plan.total
+    else:
+        begin, end = shard_range(plan.total, rank, world)
+        n = end - begin
+        key_base = begin
+        global_total = plan.total
     records = plan.generate(begin, n)
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
 
-    def merge_all(t):
-        return plan.merge(t, t.shape[0])
+    def gather(local_tab):
+        if world == 1:
+            return local_tab
+        if gloo:
+            return allgather_merge(local_tab.cpu(), lambda g: plan.merge(g.cuda(), g.shape[0]))
+        return allgather_merge(local_tab, lambda g: plan.merge(g, g.shape[0]))
 
     def step():
-        local_tab = plan.score(records, n, index_base=begin)
-        return allgather_merge(local_tab, merge_all) if world > 1 else local_tab
+        return gather(plan.score(records, n, index_base=key_base))
 
     def barrier():
         if world > 1:
             dist.barrier()
 
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if gloo else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     for _ in range(args.warmup):
         out = step()
     torch.cuda.synchronize()
     barrier()
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(torch.cuda.current_device())
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with sampler:
         torch.cuda.synchronize()
@@ -339,12 +368,8 @@ def main():
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier()
-    ms = ev0.elapsed_time(ev1) / args.steps
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    value = plan.total / (ms_max / 1e3)
+    ms_max = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    value = global_total / (ms_max / 1e3)
     final_keys = out.cpu().numpy().view(np.uint64)
 
     # --- roofline: K2 alone (partials, no merge), CUDA events on the stream ---
@@ -352,7 +377,7 @@ def main():
     k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     k0.record(stream)
     for _ in range(reps):
-        plan.score_partials(records, n, index_base=begin)
+        plan.score_partials(records, n, index_base=key_base)
     k1.record(stream)
     torch.cuda.synchronize()
     k2_ms = k0.elapsed_time(k1) / reps
@@ -363,54 +388,79 @@ def main():
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
             prof = json.load(fh)
-        if prof.get("workload") == cfg.name and prof.get("world") == world:
+        if prof.get("workload") == cfg.name and prof.get("world") == 1:
             traffic = prof.get("dram_bytes_per_launch")
     except Exception:
         pass
 
-    # --- e2e: host records through the public API ----------------------------
+    # --- e2e: the public API call a user makes (score_space on every rank) ---
+    # Per step: the space description (kernels' spaces, variant mixes, arch
+    # tables) is packed on the host and copied H2D by ScorePlan, K1 + the
+    # feature table + K2i score it on the device, the [n_seg, k] top-k
+    # tables are all-gathered and merged (N > 1), read back (D2H) and
+    # decoded into configurations.
     e2e = None
     if not args.no_e2e:
+        try:
+            e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
+            mode = args.mode
+
+            def api_step():
+                return score_space_multi(cfg.kernels, cfg.archs, mode, cfg.k,
+                                         scaling=args.scaling, gather_on_host=gloo)
+            for _ in range(2):
+                segs, keys = api_step()
+            torch.cuda.synchronize()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(e2e_steps):
+                segs, keys = api_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            e_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
+            assert np.array_equal(keys.numpy().view(np.uint64), final_keys), \
+                "API top-k differs from the record path"
+            e2e = {"value": global_total / (e_ms / 1e3), "unit": UNIT,
+                   "h2d_bytes_per_step": int(plan.h2d_bytes),
+                   "d2h_bytes_per_step": 8 * plan.n_seg * plan.k,
+                   "ms_per_step": e_ms, "steps": e2e_steps,
+                   "path": "dist.score_space_multi (= score_space() at N=1): host space "
+                           "description -> ScorePlan H2D -> K1 + feature table -> K2i "
+                           "implicit-grid score + top-k -> all-gather + K3 -> D2H -> decode"}
+        except Exception as exc:  # keep the main number; say why e2e is missing
+            e2e = {"value": None, "unit": UNIT, "error": repr(exc)[:300]}
+
+    # --- e2e from host RECORDS (PCIe-bound; N = 1 only, informational) ---------
+    e2e_records = None
+    if not args.no_e2e and world == 1:
         host = torch.empty(0)
         try:
-            e2e_steps = args.e2e_steps or max(2, min(args.steps, 5))
+            e2e_steps = max(2, min(args.steps, 3))
             host_np = np.empty(n * 16, np.uint8)
             host = torch.from_numpy(host_np)
             cudart = torch.cuda.cudart()
             cudart.cudaHostRegister(host.data_ptr(), host.numel(), 0)
             host.copy_(records[: n * 16])
-            for _ in range(1):
-                res = plan.score_host(host, n, index_base=begin)
-                if world > 1:
-                    res = allgather_merge(res, merge_all)
-                res.cpu()
+            plan.score_host(host, n, index_base=key_base).cpu()
             torch.cuda.synchronize()
-            barrier()
-            t0 = time.perf_counter()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             for _ in range(e2e_steps):
-                res = plan.score_host(host, n, index_base=begin)
-                if world > 1:
-                    res = allgather_merge(res, merge_all)
-                keys_host = res.cpu()          # D2H of the step's result
+                keys_host = plan.score_host(host, n, index_base=key_base).cpu()
             e1.record(stream)
             torch.cuda.synchronize()
             e_ms = e0.elapsed_time(e1) / e2e_steps
-            te = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
-            if world > 1:
-                dist.all_reduce(te, op=dist.ReduceOp.MAX)
-            e_ms = float(te.item())
             assert np.array_equal(keys_host.numpy().view(np.uint64), final_keys)
-            e2e = {"value": plan.total / (e_ms / 1e3), "unit": UNIT,
-                   "h2d_bytes_per_step": 16 * plan.total,
-                   "d2h_bytes_per_step": 8 * plan.n_seg * plan.k * world,
-                   "ms_per_step": e_ms, "steps": e2e_steps,
-                   "path": "ScorePlan.score_host: pinned host records -> chunked H2D "
-                           "(copy stream) overlapped with K2 -> K3 merge -> D2H top-k"}
+            e2e_records = {"value": n / (e_ms / 1e3), "unit": UNIT,
+                           "h2d_bytes_per_step": 16 * n,
+                           "d2h_bytes_per_step": 8 * plan.n_seg * plan.k,
+                           "ms_per_step": e_ms, "steps": e2e_steps,
+                           "path": "ScorePlan.score_host: pinned host records -> chunked H2D "
+                                   "(copy stream) overlapped with K2 -> K3 merge -> D2H top-k"}
             cudart.cudaHostUnregister(host.data_ptr())
-        except Exception as exc:  # keep the main number; say why e2e is missing
-            e2e = {"value": None, "unit": UNIT, "error": repr(exc)[:300]}
+        except Exception as exc:
+            e2e_records = {"value": None, "unit": UNIT, "error": repr(exc)[:300]}
 
     secondary = None
     if rank == 0 and world == 1 and not args.no_secondary:
@@ -431,24 +481,31 @@ def main():
             c_oracle = {"error": repr(exc)[:200]}
 
     if rank == 0:
+        # K2 + K3 per step, + K3 after the all-gather for N > 1
         launches = args.steps * (2 + (1 if world > 1 else 0))
+        shard = ("each GPU scores its own copy of the space" if args.scaling == "weak"
+                 else "index-range shards of one space")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "u32 integer (u64 keys)", "data": "synthetic",
-            "config": {"workload": cfg.name, "candidates": plan.total, "segments": plan.n_seg,
+            "config": {"workload": cfg.name, "candidates": global_total,
+                       "candidates_per_gpu": n, "segments": plan.n_seg,
                        "k": plan.k, "mode": args.mode, "record_bytes": 16,
                        "kernels": list(workloads.KERNEL_NAMES),
                        "archs": [a.name for a in cfg.archs],
-                       "parallelism": f"index-range shards x{world} + NCCL all-gather top-k",
-                       "l2": f"inputs {16 * plan.total / 1e9:.1f} GB >> 126 MB L2; no flush"},
+                       "parallelism": f"{shard} x{world} + "
+                                      f"{'gloo' if gloo else 'NCCL'} all-gather top-k + K3 merge",
+                       "l2": f"inputs {16 * n / 1e9:.1f} GB per GPU >> 126 MB L2; no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak,
                          "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                          "kernel": "score_topk_kernel (K2)", "kernel_ms": k2_ms,
                          "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src},
             "e2e": e2e, "gpu_launches": launches, "clocks": sampler.summary(),
         }
+        if e2e_records is not None:
+            line["e2e_records"] = e2e_records
         if secondary is not None:
             line["secondary"] = secondary
         if cpu is not None:

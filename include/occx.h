@@ -252,11 +252,14 @@ int occx_topk_merge(const occx_ctx* ctx, const uint64_t* d_lists,
  * occx_gen_space and scoring them with occx_score_topk (index_base = begin),
  * without materialising records: each candidate is decoded from its global
  * index inside the scorer (enumerate_space order, tuning.py:75-77).
- * Segment blocks (|REGS| x |SMEM|) must be < 2^32 candidates.            */
+ * Segment blocks (|REGS| x |SMEM|) must be < 2^32 candidates.
+ * key_offset is added to every candidate's global index in its key (0 for
+ * the plain space; r * total when rank r of a weak-scaling run scores its
+ * own copy of the space, so keys stay unique across ranks).             */
 int occx_score_space(const occx_ctx* ctx, const occx_arch_t* h_archs, int n_arch,
                      const occx_segdesc_t* d_desc, uint32_t n_desc,
                      const uint32_t* d_pool, uint32_t n_pool, uint64_t begin,
-                     uint64_t n, int mode, const occx_vent_t* d_vtab, uint32_t n_var,
+                     uint64_t n, uint64_t key_offset, int mode, const occx_vent_t* d_vtab, uint32_t n_var,
                      uint32_t n_seg, uint32_t k, void* d_ws, uint64_t ws_bytes,
                      uint64_t* d_topk, void* stream);
 

@@ -77,7 +77,8 @@ SIGNATURES = {
     "occx_sass_signature": ([_P, _U32], ctypes.c_char_p),
     "occx_sass_error_text": ([_P], ctypes.c_char_p),
     "occx_sass_free": ([_P], None),
-    "occx_score_space": ([_P, _P, _I, _P, _U32, _P, _U32, _U64, _U64, _I, _P, _U32, _U32, _U32,
+    "occx_score_space": ([_P, _P, _I, _P, _U32, _P, _U32, _U64, _U64, _U64, _I, _P, _U32, _U32,
+                          _U32,
                           _P, _U64, _P, _P], _I),
 }
 

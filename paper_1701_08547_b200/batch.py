@@ -316,6 +316,19 @@ def pack_mixes(mixes: Sequence[InstructionMix]) -> np.ndarray:
     return out
 
 
+def _nonneg_ints(vals) -> np.ndarray:
+    """A space dimension's values as int64 (clamped to 2^32-1); they must be
+    non-negative Python/numpy ints."""
+    arr = np.asarray(vals)
+    if arr.dtype.kind not in "iu" or arr.ndim != 1:
+        if any((not isinstance(v, int)) or v < 0 for v in vals):
+            raise ValueError("TC/BC/REGS/SMEM values must be non-negative ints")
+        return np.asarray([min(int(v), U32_MAX) for v in vals], np.int64)
+    if arr.size and arr.min() < 0:
+        raise ValueError("TC/BC/REGS/SMEM values must be non-negative ints")
+    return arr.astype(np.int64)
+
+
 def cost_key_of_cc(cc: float) -> int:
     return COST_KEY_OF_MAJOR.get(int(cc), -1)
 
@@ -476,8 +489,10 @@ class ScorePlan:
             mixes += list(kern.mixes)
             var_kernel += [ki] * len(kern.mixes)
         self.n_var = len(mixes)
-        # segments: descriptors + value pool + masks
-        pool: list[int] = []
+        # segments: descriptors + value pool + masks.  The value pool of a
+        # kernel's seven dimensions is shared by its n_arch segments.
+        pool_parts: list[np.ndarray] = []
+        n_pool = 0
         desc = np.zeros(self.n_seg, _lib.SEGDESC)
         masks = np.zeros((self.n_seg, 3), np.uint64)
         cands = [thread_candidates(a) for a in self.archs]
@@ -495,23 +510,23 @@ class ScorePlan:
             smem = extras.get("SMEM", (kern.static_shared_mem,))
             dims = [sp.thread_counts, sp.block_counts, sp.unroll_factors, sp.l1_sizes_kb,
                     sp.compiler_flags, regs, smem]
-            for vals in (dims[0], dims[1], dims[5], dims[6]):
-                if any((not isinstance(v, int)) or v < 0 for v in vals):
-                    raise ValueError("TC/BC/REGS/SMEM values must be non-negative ints")
+            offs, lens = [], []
+            for j, vals in enumerate(dims):
+                offs.append(n_pool)
+                lens.append(len(vals))
+                if j in (0, 1, 5, 6):          # value dims; UIF/PL/CFLAGS by index
+                    arr = _nonneg_ints(vals)
+                    pool_parts.append(np.minimum(arr, U32_MAX).astype(np.uint32))
+                else:
+                    pool_parts.append(np.zeros(len(vals), np.uint32))
+                n_pool += len(vals)
+            size = grid_size(sp)
+            seg_dims = [tuple(v) for _, v in sp._dimensions()]
             for a in range(self.n_arch):
                 s = ki * self.n_arch + a
-                size = grid_size(sp)
-                offs, lens = [], []
-                for j, vals in enumerate(dims):
-                    offs.append(len(pool))
-                    lens.append(len(vals))
-                    if j in (0, 1, 5, 6):      # value dims; UIF/PL/CFLAGS by index
-                        pool += [min(int(v), U32_MAX) for v in vals]
-                    else:
-                        pool += [0] * len(vals)
                 desc[s] = (start, size, a, self.var_base[ki], offs, lens)
                 self.seg_start.append(start)
-                self.seg_dims.append([tuple(v) for _, v in sp._dimensions()])
+                self.seg_dims.append(seg_dims)
                 start += size
                 masks[s] = membership_masks(sp, cands[a])
         self.total = start
@@ -519,21 +534,31 @@ class ScorePlan:
             raise DeviceError("search space above 2^34 candidates")
         self.var_kernel = np.asarray(var_kernel, np.uint32)
         self.mixes = mixes
-        torch = _torch()
-        self.d_desc = _to_device(desc)
+        self._seg_start_np = np.asarray(self.seg_start, np.int64)
+        pool = np.concatenate(pool_parts) if pool_parts else np.zeros(1, np.uint32)
         self.n_pool = max(len(pool), 1)
-        self.d_pool = _to_device(np.asarray(pool or [0], np.uint32))
+        # one H2D copy of the whole space description, carved into views
+        parts = [desc.view(np.uint8).ravel(), pool.view(np.uint8).ravel(),
+                 masks.view(np.uint8).ravel(), self.var_kernel.view(np.uint8).ravel(),
+                 pack_mixes(mixes).view(np.uint8).ravel()]
+        offsets, total_b = [], 0
+        for part in parts:
+            offsets.append(total_b)
+            total_b += -(-max(part.size, 1) // 256) * 256
+        blob = np.zeros(total_b, np.uint8)
+        for o, part in zip(offsets, parts):
+            blob[o:o + part.size] = part
+        self._d_blob = _to_device(blob)
+        views = [self._d_blob[o:] for o in offsets]
+        self.d_desc, self.d_pool, self.d_masks, self.d_var_kernel, d_mix = views
+        # bytes this plan copied host -> device (the space description; the
+        # arch rows and CPI table travel in the kernel parameter blocks)
+        self.h2d_bytes = int(blob.nbytes + self.h_archs.nbytes + 4 * 16 * 8)
         # K1 on device, then the feature table
         cols = [int(a["cost_key"]) for a in self.h_archs]
-        d_mix = _to_device(pack_mixes(mixes))
         self.d_sum, self.d_feat = feature_records(d_mix, self.n_var, cols, table.cpi_matrix(),
                                                   scale)
         self.d_vtab = _empty(self.n_var * self.n_arch * _lib.VENT.itemsize)
-        # keep every input tensor referenced until after the launch: a
-        # temporary freed before the call would be recycled by the next
-        # allocation and overwritten before the kernel reads it
-        self.d_var_kernel = _to_device(self.var_kernel)
-        self.d_masks = _to_device(masks)
         _lib.check(_lib.load().occx_build_vtab(
             _lib.ctx(), _lib.ptr(self.d_sum), _lib.ptr(self.d_feat), self.n_var, self.n_arch,
             _lib.ptr(self.d_var_kernel), _lib.ptr(self.d_masks),
@@ -544,7 +569,6 @@ class ScorePlan:
         self.ws_bytes = ws.value
         self.d_ws = _empty(self.ws_bytes)
         self.masks = masks
-        del torch
 
     # -- candidates ---------------------------------------------------------
     def generate(self, begin: int = 0, n: int | None = None, out=None):
@@ -616,17 +640,19 @@ class ScorePlan:
         return self.merge(tables, n_chunks)
 
     def score_implicit(self, begin: int = 0, n: int | None = None, out=None, stream=None,
-                       merge: bool = True):
+                       merge: bool = True, key_offset: int = 0):
         """K2i: score candidates [begin, begin+n) of the space decoded from their
         global index inside the kernel (no records in HBM).  Identical keys to
-        generate() + score(); returns the device [n_seg, k] table."""
+        generate() + score(); returns the device [n_seg, k] table.
+        ``key_offset`` shifts the index carried in the keys (a weak-scaling
+        rank scoring its own copy of the space)."""
         torch = _torch()
         n = self.total - begin if n is None else n
         if merge and out is None:
             out = torch.empty((self.n_seg, self.k), dtype=torch.int64, device="cuda")
         _lib.check(_lib.load().occx_score_space(
             _lib.ctx(), _lib.ptr(self.h_archs), self.n_arch, _lib.ptr(self.d_desc), self.n_seg,
-            _lib.ptr(self.d_pool), self.n_pool, begin, n, MODE_CODE[self.mode],
+            _lib.ptr(self.d_pool), self.n_pool, begin, n, key_offset, MODE_CODE[self.mode],
             _lib.ptr(self.d_vtab), self.n_var, self.n_seg, self.k, _lib.ptr(self.d_ws),
             self.ws_bytes, _lib.ptr(out) if merge else None, _lib.stream_ptr(stream)),
             "occx_score_space")
@@ -655,29 +681,42 @@ class ScorePlan:
         return s, tuple(reversed(digits))
 
     def decode(self, keys) -> list[SegmentTopK]:
+        """[n_seg, k] keys -> per-segment Ranked entries (host).  The key
+        fields are unpacked with numpy; each entry's space tuple comes from
+        its mixed-radix digits (enumerate_space order, last dimension
+        fastest).  Indices of weak-scaling copies are taken modulo total."""
         keys = np.asarray(keys.cpu().numpy() if hasattr(keys, "cpu") else keys).view(np.uint64)
         keys = keys.reshape(self.n_seg, self.k)
+        idx = (np.uint64(IDX_MASK) - (keys & np.uint64(IDX_MASK))).astype(np.int64)
+        local = (idx % self.total) - self._seg_start_np[:, None]
+        aw = ((keys >> np.uint64(54)) & np.uint64(0x7F)).astype(np.int64).tolist()
+        rk = ((keys >> np.uint64(34)) & np.uint64(0xFFFFF)).astype(np.int64).tolist()
+        rule = ((keys >> np.uint64(62)) & np.uint64(1)).astype(bool).tolist()
+        stat = ((keys >> np.uint64(61)) & np.uint64(1)).astype(bool).tolist()
+        nz = (keys != 0).tolist()
+        idx_l, local_l, keys_l = idx.tolist(), local.tolist(), keys.tolist()
         out = []
         for s in range(self.n_seg):
             ki, a = divmod(s, self.n_arch)
+            dims = self.seg_dims[s]
+            lens = [len(v) for v in dims]
+            nd = len(dims)
+            n_cf = lens[4]
+            vb = self.var_base[ki]
             entries = []
-            for key in keys[s]:
-                key = int(key)
-                if key == 0:
+            for j in range(self.k):
+                if not nz[s][j]:
                     continue
-                d = decode_key(key)
-                seg, cfg = self.locate(d["index"])
-                kern = self.kernels[ki]
-                sp = kern.space
-                i_u = sp.unroll_factors.index(cfg[2])
-                i_c = sp.compiler_flags.index(cfg[4])
+                rem = local_l[s][j]
+                dig = [0] * nd
+                for d in range(nd - 1, -1, -1):
+                    rem, dig[d] = divmod(rem, lens[d])
+                rbits = rk[s][j]
                 entries.append(Ranked(
-                    index=d["index"], config=cfg,
-                    variant=self.var_base[ki] + i_u * len(sp.compiler_flags) + i_c,
-                    arch=a, active_warps=d["active_warps"], rule_keep=d["rule_keep"],
-                    static_keep=d["static_keep"],
-                    cost_rank=((1 << 20) - 1 - d["rank_bits"]) if d["rank_bits"] else None,
-                    key=key))
+                    index=idx_l[s][j], config=tuple(dims[d][dig[d]] for d in range(nd)),
+                    variant=vb + dig[2] * n_cf + dig[4], arch=a,
+                    active_warps=aw[s][j], rule_keep=rule[s][j], static_keep=stat[s][j],
+                    cost_rank=((1 << 20) - 1 - rbits) if rbits else None, key=keys_l[s][j]))
             out.append(SegmentTopK(self.kernels[ki].name, self.archs[a].name, entries))
         return out
 

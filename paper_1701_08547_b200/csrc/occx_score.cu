@@ -362,6 +362,9 @@ struct SpaceParams {
   const uint32_t* pool;
   uint32_t n_desc, n_pool, pool_smem, pad;
   uint64_t begin;        // global index of the first candidate scored
+  uint64_t key_off;      // added to the global index in keys (weak-scaling copies)
+  uint32_t sep_words;    // per-warp separable-table capacity (0: general path only)
+  uint32_t pad2;
 };
 
 // Record words of the block the digits point at.
@@ -447,8 +450,107 @@ __device__ __forceinline__ uint4 ig_record(const IgCache& c, const uint32_t* poo
   return make_uint4(c.x, S, c.z, min(R, 0xffffu) | c.w_hi);
 }
 
-constexpr int kIgThreads = 768;                 // 24 warps, one CTA per SM (<= 80 registers)
+constexpr int kIgThreads = 512;                 // 16 warps, one CTA per SM (<= 128 registers)
 constexpr int kIgWarps = kIgThreads / 32;
+constexpr int kIgTab = 1024;                    // per-warp separable-table words (|REGS| + |SMEM|)
+
+// ---- separable block tables (implicit grid) --------------------------------
+// Inside one block of the space (fixed TC, BC, UIF, PL, CFLAGS, i.e. fixed
+// (T, variant, arch)) a candidate differs from its neighbours only in (R, S),
+// and the occupancy core is separable in them (occupancy.py:176-187):
+//   blocks = min(limit_by_warps(T), limit_by_registers(T, R), limit_by_smem(S))
+//   active_warps = min(blocks * wpb, Wmp)               (occupancy.py:186)
+// and because x -> min(x * wpb, Wmp) is monotone,
+//   active_warps = min(AR(R), AS(S)),  AR = min(min(lw, lr(R)) * wpb, Wmp),
+//                                      AS = min(ls(S) * wpb, Wmp).
+// When a warp enters a block it evaluates limit_by_registers over the block's
+// REGS values and limit_by_smem over its SMEM values once (exact integer
+// restatements below) into two per-warp tables holding the key's high word
+// with the active-warps field filled in; every candidate is then scored by
+// min(TR[ri], TS[si]) -- the same key bits k2_key produces from the record.
+// A zero active-warps field (no block fits, or an illegal launch) makes the
+// key 0, exactly as in k2_key.
+
+// limit_by_registers(T, R) (occupancy.py:127-145), clamped to 255 (>= lw).
+template <int MODE>
+__device__ __forceinline__ uint32_t sep_lr(const occx_arch_t& a, uint32_t wpb, uint32_t R) {
+  const uint32_t ws = (uint32_t)a.warp_size, gran = (uint32_t)a.register_alloc_granularity;
+  const uint32_t rfs = (uint32_t)a.register_file_size, rmax = (uint32_t)a.max_regs_per_thread;
+  const uint32_t bmp = (uint32_t)a.max_blocks_per_mp;
+  if (R > rmax) return 0u;
+  if (R == 0) return bmp;
+  uint32_t v;
+  if (MODE == OCCX_MODE_CORRECTED) {
+    const uint32_t alloc = (R * ws + gran - 1) / gran * gran;            // _round_up
+    v = min(bmp, (rfs / alloc) / wpb);                                   // :144-145
+  } else {
+    v = ((gran / (R * ws)) + wpb - 1) / wpb * ((rfs + gran - 1) / gran); // :139-143
+  }
+  return min(v, 255u);
+}
+
+// limit_by_smem(S) (occupancy.py:148-160), clamped to 255.
+template <int MODE>
+__device__ __forceinline__ uint32_t sep_ls(const occx_arch_t& a, uint32_t S) {
+  const uint32_t smax = (uint32_t)a.shared_mem_per_block, bmp = (uint32_t)a.max_blocks_per_mp;
+  if (S > smax) return 0u;
+  if (S == 0) return bmp;
+  const uint32_t v = (MODE == OCCX_MODE_CORRECTED) ? min(bmp, smax / S) : (smax + S - 1) / S;
+  return min(v, 255u);
+}
+
+struct SepBlock {            // warp-uniform description of the tabled block
+  uint64_t lo;               // global index of the block's first candidate
+  uint32_t n, ns, seg;       // block size, |SMEM|, segment
+  uint32_t ts;               // shared address of TS (TR starts at the warp's table)
+  FastDiv ds;                // divide by |SMEM|
+};
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// Fill TR[0, nR) and TS[0, nS) (tr = the warp's table, shared address) for
+// the block ic points at; false (tables untouched) when it does not fit.
+template <int MODE, bool VT_SMEM>
+__device__ __forceinline__ bool sep_build(const SpaceParams& q, const K2Shared& s,
+                                          const uint32_t* pool, const IgCache& ic,
+                                          uint32_t tr, SepBlock& sb, int lane) {
+  const uint32_t ns = ic.n_s, nr = ic.blk_n / ic.n_s;
+  if (nr + ns > q.sep_words) return false;
+  K2Cache kc;
+  const uint4 r0 = make_uint4(ic.x, 0u, ic.z, ic.w_hi);       // R, S irrelevant here
+  k2_fill<VT_SMEM>(s.c, r0, kc);
+  const uint32_t a = min((ic.w_hi >> 16) & 0xffu, (uint32_t)q.sp.archs.n - 1);
+  const occx_arch_t& arch = q.sp.archs.a[a];
+  const uint32_t lw = min(kc.lw, 255u), wpb = kc.wpb, wmp = kc.wmp;
+  const uint32_t hi = kc.key_hi;
+  const bool ok = kc.ok && wpb != 0;
+  __syncwarp();                                               // previous block's readers
+  for (uint32_t i = (uint32_t)lane; i < nr; i += 32) {
+    const uint32_t R = min(pool[ic.r_off + i], 0xffffu);     // record clamp (ig_record)
+    const uint32_t aw = min(min(lw, sep_lr<MODE>(arch, max(wpb, 1u), R)) * wpb, wmp);
+    sts_u32(tr + 4u * i, ok ? (hi | (aw << 22)) : 0u);
+  }
+  for (uint32_t i = (uint32_t)lane; i < ns; i += 32) {
+    const uint32_t S = pool[ic.s_off + i];
+    const uint32_t aw = min(sep_ls<MODE>(arch, S) * wpb, wmp);
+    sts_u32(tr + 4u * (nr + i), ok ? (hi | (aw << 22)) : 0u);
+  }
+  __syncwarp();
+  sb.lo = ic.blk_lo;
+  sb.n = ic.blk_n;
+  sb.ns = ns;
+  sb.seg = kc.seg;
+  sb.ts = tr + 4u * nr;
+  sb.ds = ic.ds;
+  return true;
+}
 
 template <int MODE, bool VT_SMEM>
 __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid_constant__ SpaceParams q) {
@@ -457,14 +559,17 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
   const K2Shared s = k2_setup<MODE, VT_SMEM>(p, smem);
   uint64_t* stage = reinterpret_cast<uint64_t*>(const_cast<int*>(s.lock + p.n_seg)) + 1;
   stage = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(stage) + 7) & ~uintptr_t(7));
+  uint32_t* sep_tab = reinterpret_cast<uint32_t*>(stage + 32 * (OCCX_MAX_K + 1));
   const uint32_t* pool = q.pool;
   if (q.pool_smem) {
-    uint32_t* sp = reinterpret_cast<uint32_t*>(stage + 32 * (OCCX_MAX_K + 1));
+    uint32_t* sp = sep_tab + kIgWarps * q.sep_words;
     for (uint32_t i = threadIdx.x; i < q.n_pool; i += blockDim.x) sp[i] = __ldg(q.pool + i);
     pool = sp;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
+  const uint32_t tr = (uint32_t)__cvta_generic_to_shared(sep_tab) +
+                      4u * (threadIdx.x >> 5) * q.sep_words;
   const uint64_t begin = q.begin + (uint64_t)blockIdx.x * p.chunk;
   const uint64_t stop = q.begin + p.n;
   const uint64_t end = begin + p.chunk < stop ? begin + p.chunk : stop;
@@ -475,12 +580,69 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
   IgCache ic;
   ic.blk_lo = 0;
   ic.blk_n = 0;
+  SepBlock sb;
+  sb.lo = 0;
+  sb.n = 0;
   // each warp walks its own contiguous range in 128-candidate slices, so a
   // lane's block advances by +1 (digit carry) instead of being re-decoded
   const uint64_t wsz = p.chunk / kIgWarps;               // multiple of 128
   const uint64_t wb = begin + (threadIdx.x >> 5) * wsz;
   const uint64_t we = wb + wsz < end ? wb + wsz : end;
   for (uint64_t base = wb; base < we; base += 128) {
+    // fast path: the whole slice lies in the tabled block (warp-uniform)
+    bool fast = base + 128 <= we && base - sb.lo < (uint64_t)sb.n && base + 128 - sb.lo <= sb.n;
+    if (!fast && base + 128 <= we) {
+      ig_seek(q, pool, base, ic);                          // same g on every lane
+      if (base + 128 - ic.blk_lo <= (uint64_t)ic.blk_n)
+        fast = sep_build<MODE, VT_SMEM>(q, s, pool, ic, tr, sb, lane);
+    }
+    if (fast) {
+      // lane l scores candidates base + 4l + j: (ri, si) by one division,
+      // then +1 steps with a carry (|SMEM| >= 4), else one division each
+      const uint32_t o = (uint32_t)(base - sb.lo) + 4u * (uint32_t)lane;
+      uint32_t v[4];
+      if (sb.ns >= 4) {
+        uint32_t ri = fastdiv(o, sb.ds), si = o - ri * sb.ns;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (j) {
+            const bool w = ++si == sb.ns;
+            si = w ? 0u : si;
+            ri += w ? 1u : 0u;
+          }
+          v[j] = min(lds_u32(tr + 4u * ri), lds_u32(sb.ts + 4u * si));
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t ri = fastdiv(o + j, sb.ds), si = o + j - ri * sb.ns;
+          v[j] = min(lds_u32(tr + 4u * ri), lds_u32(sb.ts + 4u * si));
+        }
+      }
+      // the lane's best key: largest high word, then the smallest j (keys
+      // carry the inverse index); it passes the warp list's filter iff any
+      // of the lane's keys does
+      const uint64_t inv0 = kIdxMask - q.key_off - (base + 4u * (uint32_t)lane);
+      const uint32_t m = max(max(v[0], v[1]), max(v[2], v[3]));
+      bool any = false;
+      if (m & 0x1fc00000u) {
+        const uint32_t jb = v[0] == m ? 0u : v[1] == m ? 1u : v[2] == m ? 2u : 3u;
+        const uint64_t inv = inv0 - jb;
+        const uint64_t kb = ((uint64_t)(m | (uint32_t)(inv >> 32)) << 32) | (uint32_t)inv;
+        any = sb.seg != wl.seg || kb > wl.thr;
+      }
+      if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint64_t inv = inv0 - (uint64_t)j;
+          const uint64_t key = (v[j] & 0x1fc00000u)
+              ? (((uint64_t)(v[j] | (uint32_t)(inv >> 32)) << 32) | (uint32_t)inv) : 0ull;
+          wl_offer(key, key ? sb.seg : wl.seg, wl, lane, p.k, s.thr, s.list, s.lock);
+        }
+      }
+      continue;
+    }
+    // general path: per-lane decode (block / segment boundaries, big tables)
     const uint64_t g0 = base + lane;
     uint4 r[4];
     bool hit = true;
@@ -503,7 +665,7 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
         r[j] = g < we ? ig_record(ic, pool, g) : make_uint4(0, 0, 0, 0xffffffffu);
       }
     }
-    k2_process4<MODE, VT_SMEM>(s, cc, wl, r, kIdxMask - g0, lane, p.k);
+    k2_process4<MODE, VT_SMEM>(s, cc, wl, r, kIdxMask - q.key_off - g0, lane, p.k);
   }
   k2_stage(wl, lane, p.k, stage, threadIdx.x >> 5);
   __syncthreads();
@@ -1060,7 +1222,8 @@ extern "C" int occx_gen_space(const occx_ctx* ctx, const occx_segdesc_t* d_desc,
 extern "C" int occx_score_space(const occx_ctx* ctx, const occx_arch_t* h_archs, int n_arch,
                                 const occx_segdesc_t* d_desc, uint32_t n_desc,
                                 const uint32_t* d_pool, uint32_t n_pool, uint64_t begin,
-                                uint64_t n, int mode, const occx_vent_t* d_vtab, uint32_t n_var,
+                                uint64_t n, uint64_t key_offset, int mode,
+                                const occx_vent_t* d_vtab, uint32_t n_var,
                                 uint32_t n_seg, uint32_t k, void* d_ws, uint64_t ws_bytes,
                                 uint64_t* d_topk, void* stream) {
   if (!ctx || (mode != 0 && mode != 1) || k == 0 || k > OCCX_MAX_K || n_seg == 0 ||
@@ -1070,10 +1233,12 @@ extern "C" int occx_score_space(const occx_ctx* ctx, const occx_arch_t* h_archs,
   int st = occx_check_archs(h_archs, n_arch, &bad);
   if (st) return st;
   if (begin + n > kIdxMask + 1 || begin + n < begin) return OCCX_ERR_CAPACITY;
+  if (key_offset > kIdxMask + 1 - (begin + n)) return OCCX_ERR_CAPACITY;
   uint64_t need = 0;
   occx_score_workspace_bytes(ctx, n_seg, k, &need);
   if (d_ws == nullptr || ws_bytes < need) return OCCX_ERR_VALUE;
   SpaceParams q{};
+  q.key_off = key_offset;
   pack_archs(h_archs, n_arch, q.sp.archs);
   q.sp.n = n;
   q.sp.index_base = begin;
@@ -1087,7 +1252,7 @@ extern "C" int occx_score_space(const occx_ctx* ctx, const occx_arch_t* h_archs,
   q.n_desc = n_desc;
   q.n_pool = n_pool;
   q.begin = begin;
-  const int grid = ctx->sm_count;                         // one 768-thread CTA per SM
+  const int grid = ctx->sm_count;                         // one kIgThreads CTA per SM
   const uint64_t tile = (uint64_t)kIgWarps * 128;          // each warp walks chunk / kIgWarps
   const uint64_t tiles = (n + tile - 1) / tile;
   q.sp.chunk = ((tiles + grid - 1) / grid) * tile;
@@ -1097,6 +1262,9 @@ extern "C" int occx_score_space(const occx_ctx* ctx, const occx_arch_t* h_archs,
   q.pool_smem = (n_pool <= 8192u) ? 1u : 0u;
   if (q.pool_smem) smem += (size_t)n_pool * 4;
   if (smem > (size_t)ctx->max_smem_optin) return OCCX_ERR_CAPACITY;
+  // per-warp separable tables when they fit (else the general path only)
+  q.sep_words = smem + (size_t)kIgWarps * kIgTab * 4 <= (size_t)ctx->max_smem_optin ? kIgTab : 0;
+  smem += (size_t)kIgWarps * q.sep_words * 4;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
 #define OCCX_LAUNCH_IG(KERNEL)                                                       \
   do {                                                                               \

@@ -43,6 +43,40 @@ def allgather_merge(local_table, merge: Callable, group=None):
     return merge(gathered.view(world, n_seg, k))
 
 
+def score_space_multi(kernels, archs, mode="corrected", k: int = 16, group=None,
+                      scaling: str = "strong", gather_on_host: bool = False):
+    """The multi-GPU form of ``score_space()`` (the public API a user calls on
+    every rank): build the plan from the host-side space description (its
+    tables go H2D), score on the device with K2i, all-gather + K3 merge the
+    fixed-size top-k tables, read them back and decode.  Returns
+    ``(segments, keys)``, identical on every rank.
+
+    ``scaling="strong"``: the ranks split one space by index range.
+    ``scaling="weak"``: every rank scores its own copy of the space; copy r
+    carries global indices [r*total, (r+1)*total) so keys stay unique.
+    ``gather_on_host``: all-gather host tensors (gloo transport)."""
+    import torch.distributed as dist
+    from .batch import ScorePlan
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    plan = ScorePlan(kernels, archs, mode, k)
+    if scaling == "weak":
+        local = plan.score_implicit(0, plan.total, key_offset=rank * plan.total)
+    elif scaling == "strong":
+        begin, end = shard_range(plan.total, rank, world)
+        local = plan.score_implicit(begin, end - begin)
+    else:
+        raise ValueError("scaling must be 'strong' or 'weak'")
+    if world > 1:
+        if gather_on_host:
+            local = allgather_merge(local.cpu(), lambda g: plan.merge(g.cuda(), g.shape[0]),
+                                    group)
+        else:
+            local = allgather_merge(local, lambda g: plan.merge(g, g.shape[0]), group)
+    keys = local.cpu()
+    return plan.decode(keys), keys
+
+
 def score_space_sharded(plan, group=None, records=None, stream=None):
     """Score the plan's whole space across the ranks of ``group``; every
     rank returns the merged [n_seg, k] device table.

@@ -215,3 +215,50 @@ def test_k0_ragged_segments_vs_oracle(seed):
         view = d[4 * mis:]                 # byte view shifted by 4*mis bytes
         out = _k0_run(view, off, lut)
         _k0_check(out, rec, off, lut)
+
+
+def random_big_block_config(rng, n_arch=3, n_kern=2):
+    """Spaces whose (REGS x SMEM) blocks span many 128-candidate slices, so
+    K2i's separable-table path runs; block sizes are not multiples of 128
+    (slices straddle blocks and segments)."""
+    from paper_1701_08547_b200 import workloads
+    from paper_1701_08547_b200.batch import KernelSpec
+    from paper_1701_08547_b200.tuning import TuningSpace
+    archs = tuple(random_arch(rng, i) for i in range(n_arch))
+    kernels = []
+    for kk in range(n_kern):
+        tc = tuple(sorted(rng.sample(range(32, 2048, 32), rng.randint(1, 5))))
+        regs = tuple(rng.sample(range(0, 1100), rng.randint(20, 300)))
+        smem = tuple(rng.choice((0, 1, 1024, 6145, 49152, 232448, rng.randint(0, 1 << 25)))
+                     for _ in range(rng.randint(1, 70)))
+        space = TuningSpace(tc, tuple(rng.sample(range(1, 300), rng.randint(1, 2))),
+                            tuple(range(1, rng.randint(2, 3))), (16,),
+                            ("", "-use_fast_math")[:rng.randint(1, 2)],
+                            extra=(("REGS", regs), ("SMEM", smem)))
+        n_var = len(space.unroll_factors) * len(space.compiler_flags)
+        kernels.append(KernelSpec(f"k{kk}", space, tuple(random_mix(rng) for _ in range(n_var))))
+    return workloads.Config("random-big", tuple(kernels), archs, rng.choice((1, 5, 16, 32)))
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_big_blocks_k2i_vs_oracle(seed):
+    """K2i separable block tables (limit_by_registers over REGS, limit_by_smem
+    over SMEM, min per candidate) == the C oracle and the record path, both
+    modes, including key offsets (weak-scaling copies) and odd windows."""
+    import paper_1701_08547_b200 as P
+    rng = random.Random(5000 + seed)
+    cfg = random_big_block_config(rng, n_arch=rng.randint(1, 4), n_kern=rng.randint(1, 3))
+    for mode in ("corrected", "verbatim"):
+        prob = oracle.problem_of(cfg, verbatim=mode == "verbatim")
+        want = oracle.score_spaces(prob, oracle.spaces_of(cfg), threads=8)
+        plan = P.ScorePlan(cfg.kernels, cfg.archs, mode, k=cfg.k)
+        got_i = plan.score_implicit().cpu().numpy().view(np.uint64)
+        assert np.array_equal(got_i, want), (seed, mode, "implicit")
+        rec = plan.generate()
+        for b, n in ((0, plan.total), (rng.randrange(plan.total), None)):
+            n = plan.total - b if n is None else n
+            off = rng.choice((0, 1, 3, plan.total, 7 * plan.total + 5))
+            a = plan.score_implicit(b, n, key_offset=off).cpu().numpy()
+            r = plan.score(plan.generate(b, n), n, index_base=b + off).cpu().numpy()
+            assert np.array_equal(a, r), (seed, mode, b, n, off)
+        del rec
