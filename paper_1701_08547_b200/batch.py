@@ -302,17 +302,27 @@ _CPI_CLASS = {row: cls for cls, row in CPI_ROW.items()}
 
 
 def pack_mixes(mixes: Sequence[InstructionMix]) -> np.ndarray:
-    out = np.zeros(len(mixes), _lib.MIX)
-    out["first_key"] = U32_MAX
+    """InstructionMix objects -> occx_mix_t rows; first_key = insertion rank."""
+    n = len(mixes)
+    counts = np.zeros((n, 16), np.int64)
+    first = np.full((n, 16), U32_MAX, np.int64)
+    regs = np.zeros(n, np.int64)
+    total = np.zeros(n, np.int64)
     for i, m in enumerate(mixes):
-        for rank, (cls, n) in enumerate(m.counts.items()):
-            if n > U32_MAX:
-                raise DeviceError("per-class count above 2^32-1")
+        row_c, row_f = counts[i], first[i]
+        for rank, (cls, c) in enumerate(m.counts.items()):
             d = DEVICE_ID[cls]
-            out[i]["counts"][d] = n
-            out[i]["first_key"][d] = rank
-        out[i]["reg_operands"] = m.reg_operands
-        out[i]["n_instr"] = min(m.total_instructions, U32_MAX)
+            row_c[d] = c
+            row_f[d] = rank
+        regs[i] = m.reg_operands
+        total[i] = m.total_instructions
+    if n and counts.max() > U32_MAX:
+        raise DeviceError("per-class count above 2^32-1")
+    out = np.zeros(n, _lib.MIX)
+    out["counts"] = counts
+    out["first_key"] = first
+    out["reg_operands"] = regs
+    out["n_instr"] = np.minimum(total, U32_MAX)
     return out
 
 
@@ -429,7 +439,7 @@ class KernelSpec:
         return len(self.space.unroll_factors) * len(self.space.compiler_flags)
 
 
-@dataclass
+@dataclass(slots=True)
 class Ranked:
     """One entry of a segment's top-k list, decoded from its key."""
 
@@ -713,10 +723,9 @@ class ScorePlan:
                     rem, dig[d] = divmod(rem, lens[d])
                 rbits = rk[s][j]
                 entries.append(Ranked(
-                    index=idx_l[s][j], config=tuple(dims[d][dig[d]] for d in range(nd)),
-                    variant=vb + dig[2] * n_cf + dig[4], arch=a,
-                    active_warps=aw[s][j], rule_keep=rule[s][j], static_keep=stat[s][j],
-                    cost_rank=((1 << 20) - 1 - rbits) if rbits else None, key=keys_l[s][j]))
+                    idx_l[s][j], tuple([dims[d][dig[d]] for d in range(nd)]),
+                    vb + dig[2] * n_cf + dig[4], a, aw[s][j], rule[s][j], stat[s][j],
+                    ((1 << 20) - 1 - rbits) if rbits else None, keys_l[s][j]))
             out.append(SegmentTopK(self.kernels[ki].name, self.archs[a].name, entries))
         return out
 

@@ -515,14 +515,15 @@ __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
-// Fill TR[0, nR) and TS[0, nS) (tr = the warp's table, shared address) for
-// the block ic points at; false (tables untouched) when it does not fit.
+// Fill TR[0, nR] and TS[0, nS + 3) (tr = the warp's table, shared address)
+// for the block ic points at; TR[nR] = 0 and TS[nS + t] = TS[t] pad the
+// +1-step lookups.  False (tables untouched) when they do not fit.
 template <int MODE, bool VT_SMEM>
 __device__ __forceinline__ bool sep_build(const SpaceParams& q, const K2Shared& s,
                                           const uint32_t* pool, const IgCache& ic,
                                           uint32_t tr, SepBlock& sb, int lane) {
   const uint32_t ns = ic.n_s, nr = ic.blk_n / ic.n_s;
-  if (nr + ns > q.sep_words) return false;
+  if (nr + ns + 4 > q.sep_words) return false;
   K2Cache kc;
   const uint4 r0 = make_uint4(ic.x, 0u, ic.z, ic.w_hi);       // R, S irrelevant here
   k2_fill<VT_SMEM>(s.c, r0, kc);
@@ -537,17 +538,18 @@ __device__ __forceinline__ bool sep_build(const SpaceParams& q, const K2Shared& 
     const uint32_t aw = min(min(lw, sep_lr<MODE>(arch, max(wpb, 1u), R)) * wpb, wmp);
     sts_u32(tr + 4u * i, ok ? (hi | (aw << 22)) : 0u);
   }
-  for (uint32_t i = (uint32_t)lane; i < ns; i += 32) {
-    const uint32_t S = pool[ic.s_off + i];
+  if (lane == 0) sts_u32(tr + 4u * nr, 0u);
+  for (uint32_t i = (uint32_t)lane; i < ns + 3; i += 32) {
+    const uint32_t S = pool[ic.s_off + (i < ns ? i : i - ns)];
     const uint32_t aw = min(sep_ls<MODE>(arch, S) * wpb, wmp);
-    sts_u32(tr + 4u * (nr + i), ok ? (hi | (aw << 22)) : 0u);
+    sts_u32(tr + 4u * (nr + 1 + i), ok ? (hi | (aw << 22)) : 0u);
   }
   __syncwarp();
   sb.lo = ic.blk_lo;
   sb.n = ic.blk_n;
   sb.ns = ns;
   sb.seg = kc.seg;
-  sb.ts = tr + 4u * nr;
+  sb.ts = tr + 4u * (nr + 1);
   sb.ds = ic.ds;
   return true;
 }
@@ -588,59 +590,76 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
   const uint64_t wsz = p.chunk / kIgWarps;               // multiple of 128
   const uint64_t wb = begin + (threadIdx.x >> 5) * wsz;
   const uint64_t we = wb + wsz < end ? wb + wsz : end;
-  for (uint64_t base = wb; base < we; base += 128) {
-    // fast path: the whole slice lies in the tabled block (warp-uniform)
-    bool fast = base + 128 <= we && base - sb.lo < (uint64_t)sb.n && base + 128 - sb.lo <= sb.n;
-    if (!fast && base + 128 <= we) {
-      ig_seek(q, pool, base, ic);                          // same g on every lane
-      if (base + 128 - ic.blk_lo <= (uint64_t)ic.blk_n)
-        fast = sep_build<MODE, VT_SMEM>(q, s, pool, ic, tr, sb, lane);
+  // fast-path state: slices left in the tabled block, the lane's offset o
+  // in the block and its (REGS, SMEM) digits, their step per slice
+  uint32_t left = 0, o = 0, ri = 0, si = 0, dq = 0, dr = 0;
+  // Score the slice at `sb_base` from the block tables: lane l takes
+  // candidates sb_base + 4l + j, all inside the tabled block.
+  auto fast_slice = [&](uint64_t sb_base) {
+    uint32_t v[4];
+    if (sb.ns >= 4) {              // at most one REGS step among the lane's four
+      const uint32_t t0 = lds_u32(tr + 4u * ri), t1 = lds_u32(tr + 4u * ri + 4u);
+      const uint32_t sa = sb.ts + 4u * si;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = min(si + j < sb.ns ? t0 : t1, lds_u32(sa + 4u * j));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t rj = fastdiv(o + j, sb.ds), sj = o + j - rj * sb.ns;
+        v[j] = min(lds_u32(tr + 4u * rj), lds_u32(sb.ts + 4u * sj));
+      }
     }
-    if (fast) {
-      // lane l scores candidates base + 4l + j: (ri, si) by one division,
-      // then +1 steps with a carry (|SMEM| >= 4), else one division each
-      const uint32_t o = (uint32_t)(base - sb.lo) + 4u * (uint32_t)lane;
-      uint32_t v[4];
-      if (sb.ns >= 4) {
-        uint32_t ri = fastdiv(o, sb.ds), si = o - ri * sb.ns;
+    // Filter on the high word only: the warp list holds keys of earlier
+    // slices of this warp's forward walk (smaller indices), so a key with
+    // the list threshold's high word is always below it.  The lane's best
+    // high word is at most max(v) | inv_hi (the rare borrow case only makes
+    // this conservative); wl_offer compares exactly.
+    const uint64_t inv0 = kIdxMask - q.key_off - (sb_base + 4u * (uint32_t)lane);
+    const uint32_t m = max(max(v[0], v[1]), max(v[2], v[3]));
+    const bool any = (m & 0x1fc00000u) &&
+                     (sb.seg != wl.seg || (m | (uint32_t)(inv0 >> 32)) > (uint32_t)(wl.thr >> 32));
+    if (__any_sync(0xffffffffu, any)) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (j) {
-            const bool w = ++si == sb.ns;
-            si = w ? 0u : si;
-            ri += w ? 1u : 0u;
-          }
-          v[j] = min(lds_u32(tr + 4u * ri), lds_u32(sb.ts + 4u * si));
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t ri = fastdiv(o + j, sb.ds), si = o + j - ri * sb.ns;
-          v[j] = min(lds_u32(tr + 4u * ri), lds_u32(sb.ts + 4u * si));
-        }
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t inv = inv0 - (uint64_t)j;
+        const uint64_t key = (v[j] & 0x1fc00000u)
+            ? (((uint64_t)(v[j] | (uint32_t)(inv >> 32)) << 32) | (uint32_t)inv) : 0ull;
+        wl_offer(key, key ? sb.seg : wl.seg, wl, lane, p.k, s.thr, s.list, s.lock);
       }
-      // the lane's best key: largest high word, then the smallest j (keys
-      // carry the inverse index); it passes the warp list's filter iff any
-      // of the lane's keys does
-      const uint64_t inv0 = kIdxMask - q.key_off - (base + 4u * (uint32_t)lane);
-      const uint32_t m = max(max(v[0], v[1]), max(v[2], v[3]));
-      bool any = false;
-      if (m & 0x1fc00000u) {
-        const uint32_t jb = v[0] == m ? 0u : v[1] == m ? 1u : v[2] == m ? 2u : 3u;
-        const uint64_t inv = inv0 - jb;
-        const uint64_t kb = ((uint64_t)(m | (uint32_t)(inv >> 32)) << 32) | (uint32_t)inv;
-        any = sb.seg != wl.seg || kb > wl.thr;
-      }
-      if (__any_sync(0xffffffffu, any)) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint64_t inv = inv0 - (uint64_t)j;
-          const uint64_t key = (v[j] & 0x1fc00000u)
-              ? (((uint64_t)(v[j] | (uint32_t)(inv >> 32)) << 32) | (uint32_t)inv) : 0ull;
-          wl_offer(key, key ? sb.seg : wl.seg, wl, lane, p.k, s.thr, s.list, s.lock);
+    }
+    o += 128;
+    si += dr;
+    ri += dq;
+    if (si >= sb.ns) {
+      si -= sb.ns;
+      ++ri;
+    }
+  };
+  for (uint64_t base = wb; base < we; base += 128) {
+    if (base + 128 <= we) {
+      ig_seek(q, pool, base, ic);                          // same g on every lane
+      if (base + 128 - ic.blk_lo <= (uint64_t)ic.blk_n &&
+          sep_build<MODE, VT_SMEM>(q, s, pool, ic, tr, sb, lane)) {
+        const uint64_t lb = (sb.lo + sb.n - base) >> 7, lr = (we - base) >> 7;
+        left = (uint32_t)(lb < lr ? lb : lr);
+        o = (uint32_t)(base - sb.lo) + 4u * (uint32_t)lane;
+        ri = fastdiv(o, sb.ds);
+        si = o - ri * sb.ns;
+        dq = 128u / sb.ns;
+        dr = 128u - dq * sb.ns;
+        // tight loop over the block's whole slices, two per trip
+        for (; left >= 2; left -= 2, base += 256) {
+          fast_slice(base);
+          fast_slice(base + 128);
         }
+        if (left) {
+          fast_slice(base);
+          left = 0;
+          base += 128;
+        }
+        base -= 128;                                       // the for-increment
+        continue;
       }
-      continue;
     }
     // general path: per-lane decode (block / segment boundaries, big tables)
     const uint64_t g0 = base + lane;
