@@ -219,32 +219,28 @@ def secondary_config3(hbm_peak: float):
             "l2": "512 MB buffer written between launches (flush)"}
 
 
-def secondary_space_api(cfg, mode: str, steps: int = 5):
-    """score_space() from host TuningSpace objects: the implicit-grid scorer
-    (K2i) decodes every candidate from its index; per call the host packs
-    the space description, H2D-copies it and reads the top-k back."""
+def secondary_space_api(cfg, mode: str, steps: int = 10):
+    """K2i, the kernel under score_space() (the e2e path): candidates decoded
+    from their index, separable per-block limit tables.  No
+    candidate bytes in HBM, so its bound is integer issue, not bandwidth;
+    the ncu capture in profiles/ gives the issue / ALU-pipe utilisation."""
     import torch
-    from paper_1701_08547_b200 import ScorePlan, score_space
+    from paper_1701_08547_b200 import ScorePlan
     plan = ScorePlan(cfg.kernels, cfg.archs, mode, k=cfg.k)
     for _ in range(3):
-        plan.score_implicit()
+        plan.score_implicit(merge=False)
     torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
+    e0.record(stream)
     for _ in range(steps):
-        plan.score_implicit()
-    e1.record()
+        plan.score_implicit(merge=False)
+    e1.record(stream)
     torch.cuda.synchronize()
     k_ms = e0.elapsed_time(e1) / steps
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        score_space(cfg.kernels, cfg.archs, mode, cfg.k)
-    api_ms = (time.perf_counter() - t0) / steps * 1e3
-    return {"kernel": "score_space_kernel (K2i, implicit grid)", "kernel_ms": k_ms,
-            "kernel_value": plan.total / (k_ms / 1e3),
-            "api_ms": api_ms, "api_value": plan.total / (api_ms / 1e3), "unit": UNIT,
-            "note": "no candidate records in HBM; api_ms is wall time of score_space() "
-                    "including ScorePlan construction (K1 + feature table) and decode"}
+    return {"kernel": "score_space_kernel (K2i, implicit grid, no K3)", "kernel_ms": k_ms,
+            "value": plan.total / (k_ms / 1e3), "unit": UNIT, "bound": "integer issue",
+            "note": "no candidate records in HBM; see profiles/r01_k2i_ncu_full.json"}
 
 
 # ---------------------------------------------------------------------------
