@@ -289,7 +289,7 @@ def main():
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": None, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "int64 (Python int)", "data": "synthetic",
             "config": {"workload": cfg.name, "candidates": cfg.total, "mode": args.mode},
             "cpu_baseline": r,
