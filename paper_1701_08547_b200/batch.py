@@ -704,29 +704,39 @@ class ScorePlan:
         rule = ((keys >> np.uint64(62)) & np.uint64(1)).astype(bool).tolist()
         stat = ((keys >> np.uint64(61)) & np.uint64(1)).astype(bool).tolist()
         nz = (keys != 0).tolist()
-        idx_l, local_l, keys_l = idx.tolist(), local.tolist(), keys.tolist()
+        idx_l, keys_l = idx.tolist(), keys.tolist()
         out = []
-        for s in range(self.n_seg):
-            ki, a = divmod(s, self.n_arch)
-            dims = self.seg_dims[s]
-            lens = [len(v) for v in dims]
+        na, k = self.n_arch, self.k
+        for ki, kern in enumerate(self.kernels):
+            # the kernel's n_arch segments share its dimensions: digits of all
+            # their entries at once (numpy), configs zipped into tuples in C
+            dims = self.seg_dims[ki * na]
             nd = len(dims)
-            n_cf = lens[4]
-            vb = self.var_base[ki]
-            entries = []
-            for j in range(self.k):
-                if not nz[s][j]:
-                    continue
-                rem = local_l[s][j]
-                dig = [0] * nd
-                for d in range(nd - 1, -1, -1):
-                    rem, dig[d] = divmod(rem, lens[d])
-                rbits = rk[s][j]
-                entries.append(Ranked(
-                    idx_l[s][j], tuple([dims[d][dig[d]] for d in range(nd)]),
-                    vb + dig[2] * n_cf + dig[4], a, aw[s][j], rule[s][j], stat[s][j],
-                    ((1 << 20) - 1 - rbits) if rbits else None, keys_l[s][j]))
-            out.append(SegmentTopK(self.kernels[ki].name, self.archs[a].name, entries))
+            rem = local[ki * na:(ki + 1) * na].reshape(-1).copy()
+            rem[rem < 0] = 0                                    # empty slots (key 0)
+            digs = [None] * nd
+            for d in range(nd - 1, -1, -1):
+                rem, digs[d] = np.divmod(rem, len(dims[d]))
+            cols = []
+            for d in range(nd):
+                vals = np.empty(len(dims[d]), dtype=object)
+                for i_v, v in enumerate(dims[d]):              # values kept as given
+                    vals[i_v] = v
+                cols.append(vals[digs[d]])
+            configs = list(zip(*cols))
+            variants = (self.var_base[ki] + digs[2] * len(dims[4]) + digs[4]).tolist()
+            for a in range(na):
+                s = ki * na + a
+                entries = []
+                for j in range(k):
+                    if not nz[s][j]:
+                        continue
+                    f = a * k + j
+                    rbits = rk[s][j]
+                    entries.append(Ranked(
+                        idx_l[s][j], configs[f], variants[f], a, aw[s][j], rule[s][j],
+                        stat[s][j], ((1 << 20) - 1 - rbits) if rbits else None, keys_l[s][j]))
+                out.append(SegmentTopK(kern.name, self.archs[a].name, entries))
         return out
 
 

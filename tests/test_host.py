@@ -169,3 +169,46 @@ def test_corpus_deterministic_and_sliceable():
     assert (ra >> 25).max() == 0 and ((ra >> 17) & 0xFF).max() <= 4
     lengths = np.diff(a.offsets.astype(np.int64))
     assert lengths.min() >= 32 and lengths.max() <= 32 + 1984
+
+
+def test_decode_matches_locate_on_random_keys():
+    """ScorePlan.decode (numpy digits, zipped configs) == locate() per key,
+    including weak-scaling indices beyond total and empty slots."""
+    import numpy as np
+    from paper_1701_08547_b200 import workloads
+    from paper_1701_08547_b200.batch import IDX_MASK, ScorePlan
+    cfg = workloads.config4()
+    plan = object.__new__(ScorePlan)             # host-side fields only (no GPU)
+    plan.kernels, plan.archs = list(cfg.kernels), list(cfg.archs)
+    plan.n_arch, plan.k = len(cfg.archs), 16
+    plan.n_seg = len(cfg.kernels) * plan.n_arch
+    starts, dims, vb, st, nv = [], [], [], 0, 0
+    for kern in cfg.kernels:
+        vb.append(nv)
+        nv += len(kern.mixes)
+        d = [tuple(v) for _, v in kern.space._dimensions()]
+        size = int(np.prod([len(x) for x in d]))
+        for _ in range(plan.n_arch):
+            starts.append(st)
+            dims.append(d)
+            st += size
+    plan.seg_start, plan.seg_dims, plan.total, plan.var_base = starts, dims, st, vb
+    plan._seg_start_np = np.asarray(starts, np.int64)
+    rng = np.random.default_rng(3)
+    keys = np.zeros((plan.n_seg, plan.k), np.uint64)
+    for s in range(plan.n_seg):
+        n = rng.integers(0, plan.k + 1)
+        size = (starts[s + 1] if s + 1 < plan.n_seg else st) - starts[s]
+        idx = starts[s] + rng.integers(0, size, n) + plan.total * rng.integers(0, 3, n)
+        keys[s, :n] = (np.uint64(1) << np.uint64(63)) | (np.uint64(7) << np.uint64(34)) | \
+            (np.uint64(IDX_MASK) - idx.astype(np.uint64))
+    for seg in plan.decode(keys):
+        for e in seg.entries:
+            s, cfg_t = plan.locate(e.index % plan.total)
+            assert e.config == cfg_t
+            ki = s // plan.n_arch
+            sp = plan.kernels[ki].space
+            want_v = vb[ki] + sp.unroll_factors.index(cfg_t[2]) * len(sp.compiler_flags) + \
+                sp.compiler_flags.index(cfg_t[4])
+            assert e.variant == want_v and e.cost_rank == (1 << 20) - 1 - 7
+    assert sum(len(s.entries) for s in plan.decode(keys)) == int((keys != 0).sum())
