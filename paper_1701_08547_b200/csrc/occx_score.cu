@@ -276,9 +276,13 @@ __device__ __forceinline__ void k2_process4(const K2Shared& s, K2Cache& cc, Warp
       seg[j] = cc.seg;
     }
   }
+  // branch-free filter (bitwise on bools: no short-circuit branches); a
+  // legal key has bit 63 set, so its high word alone says "non-zero"
+  const uint64_t thr = wl.thr;
   bool any = false;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) any |= key[j] != 0 && (seg[j] != wl.seg || key[j] > wl.thr);
+  for (int j = 0; j < 4; ++j)
+    any = any | (((uint32_t)(key[j] >> 32) != 0u) & ((seg[j] != wl.seg) | (key[j] > thr)));
   if (__any_sync(0xffffffffu, any)) {
 #pragma unroll
     for (int j = 0; j < 4; ++j)
@@ -780,10 +784,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
       const uint4* tile = ring + (size_t)st * kTmaTile;
       const uint32_t slice = (uint32_t)(warp - 1) * 128u + lane;
       uint4 r[4];
+      if (cnt == (uint32_t)kTmaTile) {                // every tile but the last
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t idx = slice + 32u * j;
-        r[j] = idx < cnt ? tile[idx] : make_uint4(0, 0, 0, 0xffffffffu);
+        for (int j = 0; j < 4; ++j) r[j] = tile[slice + 32u * j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t idx = slice + 32u * j;
+          r[j] = idx < cnt ? tile[idx] : make_uint4(0, 0, 0, 0xffffffffu);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);      // records are in registers
