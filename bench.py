@@ -497,7 +497,10 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak,
                          "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                          "kernel": "score_topk_kernel (K2)", "kernel_ms": k2_ms,
-                         "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src},
+                         "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src,
+                         "note": "peak is the driver's copy (read+write) bandwidth; K2 only "
+                                 "reads its 16-B records, and a read stream can exceed the copy "
+                                 "figure (ncu dram__bytes_read per launch is in traffic)"},
             "e2e": e2e, "gpu_launches": launches, "clocks": sampler.summary(),
         }
         if e2e_records is not None:
