@@ -18,7 +18,8 @@ import numpy as np
 from .errors import DeviceError, raise_status
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liboccx.so")
+# OCCX_LIB: an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("OCCX_LIB") or os.path.join(_HERE, "liboccx.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "occx.h")
 
 # --- struct layouts (must match include/occx.h) -----------------------------

@@ -19,13 +19,17 @@
 // more), so unequal kernel lengths do not leave a tail, and no kernel pads
 // its last chunk.
 //
-// Counting: the class table holds, per (signature, guard), the byte offset
-// of a 32-entry u64 increment table over sixteen 4-bit counters (class
-// nibble, plus the PredIns nibble and a "guard counted" marker in the spare
-// nibble 15 when the guard adds a PredIns), so a record costs one LDS.U8,
-// one LDS.64 and a 64-bit add.  Each piece of <= 8 records per lane is
-// folded into byte counters (even / odd classes), reduced over the warp
-// with 16-bit-lane REDUX.SUM before they can overflow.
+// Counting: the class table holds, per (signature, guard), one byte
+// 4c | 128g (c = class, g = the guard adds a PredIns); 0x7c is "not in this
+// kernel".  A record's sixteen-nibble increment (class nibble, plus the
+// PredIns nibble and a "guard counted" marker in the spare nibble 15) is
+// read from a 64-entry u64 table at byte 2 * entry for 6 of a lane's 8
+// records and computed as (1 << 4c) + g * (nibble 11 + nibble 15) for the
+// other 2: the split balances the shared-memory and ALU pipes (sweep over
+// 0/2/4/6/8 table records: 0.148/0.143/0.139/0.137/0.143 ms on config 3).
+// Each piece of <= 8 records per lane is folded into byte counters (even /
+// odd classes), reduced over the warp with 16-bit-lane REDUX.SUM before
+// they can overflow.
 // Dict insertion order (it decides the summation order of the FLOPS terms
 // in mix.py:278) is recovered as first_key[c] = min over occurrences of
 // 2*i (class of instruction i) or 2*i+1 (guard PredIns of instruction i);
@@ -44,7 +48,11 @@ constexpr uint32_t kChunk = 256;                      // records per warp-chunk 
 constexpr int kFlushPieces = 255 / 8;                 // byte counters cannot overflow
 constexpr uint32_t kPred = 11;                        // OpClass.PREDICATE device id
 constexpr uint32_t kAbsent = 0xffffffffu;
-constexpr uint32_t kNullLv = 15u << 3;                // class 15: counts nothing
+constexpr uint32_t kNullLv = 0x7cu;                   // class 15, shift 124: counts nothing
+#ifndef OCCX_K0_LDS
+#define OCCX_K0_LDS 6
+#endif
+constexpr int kLdsRecords = OCCX_K0_LDS;              // of a lane's 8 records, via the table
 
 struct MixParams {
   const uint32_t* instr;
@@ -116,13 +124,26 @@ __device__ __forceinline__ void count_piece(MixAcc& a, const uint32_t (&lv)[8],
   uint32_t h0 = 0, h1 = 0, v0 = 0, v1 = 0;        // h: records of the first row block (u = 0)
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
-    const uint2 d = *reinterpret_cast<const uint2*>(incb + lv[e]);
+    // class nibble increment 1 << 4c as a 64-bit shift (shift >= 64, the
+    // null entry, gives 0); a counted guard adds PredIns (nibble 11) and the
+    // marker (nibble 15): bit 7 of the entry times 0x10001000 >> 7
+    const uint32_t l = lv[e];
+    uint32_t dx, dy;
+    if (e < kLdsRecords) {         // shared increment table: entry at byte 2 * l
+      const uint2 d = *reinterpret_cast<const uint2*>(incb + 2u * l);
+      dx = d.x;
+      dy = d.y;
+    } else {                       // arithmetic: balances the shared-memory and ALU pipes
+      asm("{\n\t.reg .b64 t;\n\tshl.b64 t, 1, %2;\n\tmov.b64 {%0, %1}, t;\n\t}"
+          : "=r"(dx), "=r"(dy) : "r"(l & 0x7fu));
+      dy += (l & 0x80u) * 0x200020u;
+    }
     if (e < 4) {
-      h0 += d.x;
-      h1 += d.y;
+      h0 += dx;
+      h1 += dy;
     } else {
-      v0 += d.x;
-      v1 += d.y;
+      v0 += dx;
+      v1 += dy;
     }
   }
   v0 += h0;
@@ -147,7 +168,7 @@ __device__ __forceinline__ void count_piece(MixAcc& a, const uint32_t (&lv)[8],
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       if (e >= rows) break;
-      const uint32_t c = lv[e] >> 3 & 15u;
+      const uint32_t c = lv[e] >> 2 & 15u;
       const uint32_t pos = keybase + 128u * (uint32_t)(e >> 2) + 4u * (uint32_t)lane + (uint32_t)(e & 3);
       const uint32_t same = __match_any_sync(0xffffffffu, c);
       if ((same & lt) == 0) atomicMin(my_first + c, 2u * pos);   // slot 15 (padding) is never read
@@ -203,14 +224,14 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 // Shared-memory layout: [32] u64 increments | [warps][17] first positions
 // (+2 pad) | per-warp ring of kDepth chunks (kChunk records each) | class table.
-__host__ __device__ constexpr size_t mix_ring_offset() { return 32 * 8 + (kWarps * 17 + 2) * 4 + 8; }
+__host__ __device__ constexpr size_t mix_ring_offset() { return 64 * 8 + (kWarps * 17 + 2) * 4 + 8; }
 
 template <int kDepth>
 __global__ void __launch_bounds__(kMixThreads, 1) mix_reduce_kernel(const __grid_constant__ MixParams p,
                                                                      uint32_t lut_mask) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* inc = reinterpret_cast<uint64_t*>(smem);
-  uint32_t* firsts = reinterpret_cast<uint32_t*>(inc + 32);
+  uint32_t* firsts = reinterpret_cast<uint32_t*>(inc + 64);
   uint4* ring = reinterpret_cast<uint4*>(smem + mix_ring_offset());
   unsigned char* lut = reinterpret_cast<unsigned char*>(ring + (size_t)kWarps * kDepth * (kChunk / 4));
   const int lane = threadIdx.x & 31;
@@ -229,8 +250,10 @@ __global__ void __launch_bounds__(kMixThreads, 1) mix_reduce_kernel(const __grid
     ke = __shfl_sync(0xffffffffu, r, 16);
   }
 
-  for (uint32_t i = threadIdx.x; i < 32; i += blockDim.x) {
-    const uint32_t c = i & 15u, g = i >> 4;
+  // increment table indexed by class-table byte / 4 (= c + 32 * guard):
+  // entries 15..31 and 47..63 are zero (31 = the null entry)
+  for (uint32_t i = threadIdx.x; i < 64; i += blockDim.x) {
+    const uint32_t c = i & 31u, g = i >> 5;
     uint64_t v = 0;
     if (c < 15) {
       v = 1ull << (4 * c);
@@ -263,7 +286,7 @@ __global__ void __launch_bounds__(kMixThreads, 1) mix_reduce_kernel(const __grid
       const uint32_t sig = 4 * i + (uint32_t)b;
       const uint32_t c = sig < p.n_sig ? ((w4 >> (8 * b)) & 15u) : 14u;
       const uint32_t g = (c < 11 || c == 14) ? 16u : 0u;
-      const uint32_t pair = (c << 3) | ((c | g) << 11);
+      const uint32_t pair = (c << 2) | (((c << 2) | (g << 3)) << 8);   // byte: 4c | guard<<7
       if (b & 1) o[b >> 1] |= pair << 16; else o[b >> 1] = pair;
     }
     *reinterpret_cast<uint2*>(lut + 8 * i) = make_uint2(o[0], o[1]);
