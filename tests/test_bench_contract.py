@@ -1,0 +1,44 @@
+"""bench.py's JSON contract: the reference arm on CPU, and (GPU) the
+multi-rank path through torchrun with the gloo harness on one device."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(args, timeout=600, env=None):
+    r = subprocess.run([sys.executable, *args], cwd=ROOT, capture_output=True, text=True,
+                       timeout=timeout, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_reference_arm_line():
+    d = _run(["bench.py", "--impl", "reference", "--steps", "1", "--warmup", "3",
+              "--workload", "config4", "--cpu-sample", "40000"])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "candidates/s"
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}
+    assert d["higher_is_better"] is True and d["scaling"] == "weak"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scaling", ["weak", "strong"])
+def test_two_rank_bench_line_gloo_harness(scaling):
+    d = _run(["-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+              "--master-addr", "127.0.0.1", "--master-port", "29611" if scaling == "weak" else "29612",
+              "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3", "--dist-backend", "gloo",
+              "--workload", "config4", "--no-cpu", "--scaling", scaling], timeout=900)
+    assert d["n_gpus"] == 2 and d["scaling"] == scaling
+    per = d["config"]["candidates_per_gpu"]
+    assert d["config"]["candidates"] == (2 * per if scaling == "weak" else 104_857_600)
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] == 3 * 3
+    assert d["roofline"]["bound"] == "hbm" and d["clocks"]["sm_max_mhz"]
