@@ -164,17 +164,25 @@ __device__ __forceinline__ void count_piece(MixAcc& a, const uint32_t (&lv)[8],
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
     const uint32_t first_lo = __reduce_or_sync(0xffffffffu, nibble_presence(h0));
     const uint32_t first_hi = __reduce_or_sync(0xffffffffu, nibble_presence(h1));
+    // rows of block 0 only when a new class occurs there, of block 1 only
+    // when one is absent from block 0 (a piece may start or end mid-chunk);
+    // the guard rows only while no counted guard has been seen (nibble 15)
+    const int row0 = ((new_lo & first_lo) | (new_hi & first_hi)) ? 0 : 4;
     const int rows = ((new_lo & ~first_lo) | (new_hi & ~first_hi)) ? 8 : 4;
+    const bool guard_new = (new_hi & 0x10000000u) != 0u;
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       if (e >= rows) break;
+      if (e < row0) continue;
       const uint32_t c = lv[e] >> 2 & 15u;
       const uint32_t pos = keybase + 128u * (uint32_t)(e >> 2) + 4u * (uint32_t)lane + (uint32_t)(e & 3);
       const uint32_t same = __match_any_sync(0xffffffffu, c);
       if ((same & lt) == 0) atomicMin(my_first + c, 2u * pos);   // slot 15 (padding) is never read
       // guard PredIns (non-CTRL class): key 2*pos + 1, tracked in slot 16
-      const uint32_t gb = __ballot_sync(0xffffffffu, lv[e] & 128u);
-      if ((lv[e] & 128u) && (gb & lt) == 0) atomicMin(my_first + 16, 2u * pos + 1);
+      if (guard_new) {
+        const uint32_t gb = __ballot_sync(0xffffffffu, lv[e] & 128u);
+        if ((lv[e] & 128u) && (gb & lt) == 0) atomicMin(my_first + 16, 2u * pos + 1);
+      }
     }
   }
   a.be0 += v0 & 0x0f0f0f0fu;
