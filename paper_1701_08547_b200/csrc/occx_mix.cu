@@ -64,20 +64,30 @@ struct MixParams {
 };
 
 // Sum 16 byte counters held as even classes (w[0] classes 0,2,4,6; w[1]
-// 8,10,12,14) and odd classes (w[2] 1,3,5,7; w[3] 9,11,13,15); lane c < 16
-// receives class c's total.  16-bit lanes: 32 x 255 < 2^16.
+// 8,10,12,14) and odd classes (w[2] 1,3,5,7; w[3] 9,11,13,15) over the
+// warp; lane c < 16 adds class c's total to `total`.  16-bit lanes: 32 x
+// 255 < 2^16.  The eight warp sums (uniform) go through the warp's 8-word
+// scratch so each lane picks its own 16-bit half with one LDS.U16.
 __device__ __forceinline__ void reduce_counters_eo(const uint32_t (&w)[4], int lane,
-                                                   uint32_t& total) {
+                                                   uint32_t& total, uint32_t* xch) {
+  uint32_t r[8];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const uint32_t lo = __reduce_add_sync(0xffffffffu, w[q] & 0x00ff00ffu);   // bytes 0, 2
-    const uint32_t hi = __reduce_add_sync(0xffffffffu, (w[q] >> 8) & 0x00ff00ffu);  // bytes 1, 3
-    const int base = (q & 1) * 8 + (q >> 1);             // class of byte 0 in this word
-    if (lane == base) total += lo & 0xffffu;
-    if (lane == base + 2) total += hi & 0xffffu;
-    if (lane == base + 4) total += lo >> 16;
-    if (lane == base + 6) total += hi >> 16;
+    r[2 * q] = __reduce_add_sync(0xffffffffu, w[q] & 0x00ff00ffu);            // bytes 0, 2
+    r[2 * q + 1] = __reduce_add_sync(0xffffffffu, (w[q] >> 8) & 0x00ff00ffu);  // bytes 1, 3
   }
+  if (lane == 0) {
+    reinterpret_cast<uint4*>(xch)[0] = make_uint4(r[0], r[1], r[2], r[3]);
+    reinterpret_cast<uint4*>(xch)[1] = make_uint4(r[4], r[5], r[6], r[7]);
+  }
+  __syncwarp();
+  // class c: word q = 2*(c & 1) + (c >> 3), byte b = (c >> 1) & 3 -> u16
+  // index 4q + 2(b & 1) + (b >> 1)
+  const uint32_t c = (uint32_t)lane & 15u, b = (c >> 1) & 3u;
+  const uint32_t idx = 4u * (2u * (c & 1u) + (c >> 3)) + 2u * (b & 1u) + (b >> 1);
+  const uint32_t v = reinterpret_cast<const uint16_t*>(xch)[idx];
+  __syncwarp();
+  total += v;
 }
 
 // lower_bound: smallest k in [0, n] with off[k] >= bound (off[n] >= bound
@@ -192,7 +202,7 @@ __device__ __forceinline__ void count_piece(MixAcc& a, const uint32_t (&lv)[8],
   if (++a.pieces == kFlushPieces) {
     a.pieces = 0;
     const uint32_t w[4] = {a.be0, a.be1, a.bo0, a.bo1};
-    reduce_counters_eo(w, lane, a.total);
+    reduce_counters_eo(w, lane, a.total, my_first + 24);
     a.be0 = a.be1 = a.bo0 = a.bo1 = 0;
   }
 }
@@ -201,9 +211,8 @@ __device__ __forceinline__ void finish_kernel(MixAcc& a, uint32_t* my_first, occ
                                               uint32_t n_instr, int lane) {
   {
     const uint32_t w[4] = {a.be0, a.be1, a.bo0, a.bo1};
-    reduce_counters_eo(w, lane, a.total);
+    reduce_counters_eo(w, lane, a.total, my_first + 24);
   }
-  __syncwarp();
   uint32_t first = lane < 17 ? my_first[lane] : kAbsent;
   const uint32_t gfirst = __shfl_sync(0xffffffffu, first, 16);
   if (lane == (int)kPred && gfirst < first) first = gfirst;
@@ -230,9 +239,10 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Shared-memory layout: [32] u64 increments | [warps][17] first positions
-// (+2 pad) | per-warp ring of kDepth chunks (kChunk records each) | class table.
-__host__ __device__ constexpr size_t mix_ring_offset() { return 64 * 8 + (kWarps * 17 + 2) * 4 + 8; }
+// Shared-memory layout: [64] u64 increments | [warps][32] first positions
+// (slots 0-16) and reduction scratch (24-31) | per-warp ring of kDepth chunks (kChunk records each) | class table.
+constexpr int kFirstStride = 32;                      // per warp: 17 first slots, 8-word scratch at 24
+__host__ __device__ constexpr size_t mix_ring_offset() { return 64 * 8 + kWarps * kFirstStride * 4; }
 
 template <int kDepth>
 __global__ void __launch_bounds__(kMixThreads, 1) mix_reduce_kernel(const __grid_constant__ MixParams p,
@@ -269,7 +279,7 @@ __global__ void __launch_bounds__(kMixThreads, 1) mix_reduce_kernel(const __grid
     }
     inc[i] = v;
   }
-  for (uint32_t i = threadIdx.x; i < kWarps * 17; i += blockDim.x) firsts[i] = kAbsent;
+  for (uint32_t i = threadIdx.x; i < kWarps * kFirstStride; i += blockDim.x) firsts[i] = kAbsent;
   // class table indexed by the record's low 17 bits (sig << 1 | guard) and
   // the mask lut_mask (power of two - 1 >= 2*n_sig + 1): entry = 8 * (class
   // | 16 when the guard adds a PredIns), i.e. the byte offset of the
@@ -302,7 +312,7 @@ __global__ void __launch_bounds__(kMixThreads, 1) mix_reduce_kernel(const __grid
   __syncthreads();
   if (ks >= ke) return;
   const unsigned char* incb = reinterpret_cast<const unsigned char*>(inc);
-  uint32_t* my_first = firsts + (threadIdx.x >> 5) * 17;
+  uint32_t* my_first = firsts + (threadIdx.x >> 5) * kFirstStride;
 
   // Positions are kept relative to the warp's first chunk start cs0 (u32:
   // a call holds < 2^32 records).  The chunk grid is aligned to 16-byte
