@@ -532,13 +532,17 @@ class ScorePlan:
                 n_pool += len(vals)
             size = grid_size(sp)
             seg_dims = [tuple(v) for _, v in sp._dimensions()]
+            mask_of: dict = {}                 # archs sharing T* share the masks
             for a in range(self.n_arch):
                 s = ki * self.n_arch + a
                 desc[s] = (start, size, a, self.var_base[ki], offs, lens)
                 self.seg_start.append(start)
                 self.seg_dims.append(seg_dims)
                 start += size
-                masks[s] = membership_masks(sp, cands[a])
+                m = mask_of.get(cands[a])
+                if m is None:
+                    m = mask_of[cands[a]] = membership_masks(sp, cands[a])
+                masks[s] = m
         self.total = start
         if self.total > IDX_MASK + 1:
             raise DeviceError("search space above 2^34 candidates")
@@ -690,11 +694,31 @@ class ScorePlan:
             digits.append(vals[r])
         return s, tuple(reversed(digits))
 
+    def decode_tables(self) -> list:
+        """Key-independent part of decode (per kernel: its dimensions as
+        object arrays for fancy indexing); cached on the plan, so the API
+        can build it while the GPU scores."""
+        tabs = getattr(self, "_decode_tabs", None)
+        if tabs is None:
+            tabs = []
+            for ki in range(len(self.kernels)):
+                dims = self.seg_dims[ki * self.n_arch]
+                cols = []
+                for vals_in in dims:
+                    vals = np.empty(len(vals_in), dtype=object)
+                    for i_v, v in enumerate(vals_in):           # values kept as given
+                        vals[i_v] = v
+                    cols.append(vals)
+                tabs.append((dims, cols))
+            self._decode_tabs = tabs
+        return tabs
+
     def decode(self, keys) -> list[SegmentTopK]:
         """[n_seg, k] keys -> per-segment Ranked entries (host).  The key
         fields are unpacked with numpy; each entry's space tuple comes from
         its mixed-radix digits (enumerate_space order, last dimension
         fastest).  Indices of weak-scaling copies are taken modulo total."""
+        tabs = self.decode_tables()
         keys = np.asarray(keys.cpu().numpy() if hasattr(keys, "cpu") else keys).view(np.uint64)
         keys = keys.reshape(self.n_seg, self.k)
         idx = (np.uint64(IDX_MASK) - (keys & np.uint64(IDX_MASK))).astype(np.int64)
@@ -710,20 +734,14 @@ class ScorePlan:
         for ki, kern in enumerate(self.kernels):
             # the kernel's n_arch segments share its dimensions: digits of all
             # their entries at once (numpy), configs zipped into tuples in C
-            dims = self.seg_dims[ki * na]
+            dims, vcols = tabs[ki]
             nd = len(dims)
             rem = local[ki * na:(ki + 1) * na].reshape(-1).copy()
             rem[rem < 0] = 0                                    # empty slots (key 0)
             digs = [None] * nd
             for d in range(nd - 1, -1, -1):
                 rem, digs[d] = np.divmod(rem, len(dims[d]))
-            cols = []
-            for d in range(nd):
-                vals = np.empty(len(dims[d]), dtype=object)
-                for i_v, v in enumerate(dims[d]):              # values kept as given
-                    vals[i_v] = v
-                cols.append(vals[digs[d]])
-            configs = list(zip(*cols))
+            configs = list(zip(*[vcols[d][digs[d]] for d in range(nd)]))
             variants = (self.var_base[ki] + digs[2] * len(dims[4]) + digs[4]).tolist()
             for a in range(na):
                 s = ki * na + a
@@ -761,4 +779,6 @@ def score_space(kernels: Sequence[KernelSpec], archs: Sequence[ArchSpec],
     from their index inside the scorer (K2i): nothing but the space
     description, the feature table and the top-k table touch HBM."""
     plan = ScorePlan(kernels, archs, mode, k)
-    return plan.decode(plan.score_implicit())
+    keys = plan.score_implicit()
+    plan.decode_tables()               # host work while the GPU scores
+    return plan.decode(keys)
