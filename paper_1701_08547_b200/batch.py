@@ -505,6 +505,9 @@ class ScorePlan:
         n_pool = 0
         desc = np.zeros(self.n_seg, _lib.SEGDESC)
         masks = np.zeros((self.n_seg, 3), np.uint64)
+        d_rows: list = []
+        d_offs: list = []
+        d_lens: list = []
         cands = [thread_candidates(a) for a in self.archs]
         self.seg_start: list[int] = []
         self.seg_dims: list[list[tuple]] = []
@@ -535,7 +538,9 @@ class ScorePlan:
             mask_of: dict = {}                 # archs sharing T* share the masks
             for a in range(self.n_arch):
                 s = ki * self.n_arch + a
-                desc[s] = (start, size, a, self.var_base[ki], offs, lens)
+                d_rows.append((start, size, a, self.var_base[ki]))
+                d_offs.append(offs)
+                d_lens.append(lens)
                 self.seg_start.append(start)
                 self.seg_dims.append(seg_dims)
                 start += size
@@ -543,6 +548,12 @@ class ScorePlan:
                 if m is None:
                     m = mask_of[cands[a]] = membership_masks(sp, cands[a])
                 masks[s] = m
+        if d_rows:                             # descriptor columns in one go
+            cols = np.asarray(d_rows, np.uint64)
+            desc["start"], desc["size"] = cols[:, 0], cols[:, 1]
+            desc["arch"], desc["var_base"] = cols[:, 2], cols[:, 3]
+            desc["dim_off"] = np.asarray(d_offs, np.uint32)
+            desc["dim_len"] = np.asarray(d_lens, np.uint32)
         self.total = start
         if self.total > IDX_MASK + 1:
             raise DeviceError("search space above 2^34 candidates")
