@@ -1,0 +1,82 @@
+"""The C ABI's argument checks on a real device: every rejected call returns
+the documented status (include/occx.h) and launches nothing; the Python
+layer maps statuses onto the reference's exception classes."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    from paper_1701_08547_b200 import ScorePlan, _lib, workloads
+    cfg = workloads.config1()
+    plan = ScorePlan(cfg.kernels, cfg.archs, k=cfg.k)
+    rec = plan.generate()
+    return torch, _lib, _lib.load(), plan, rec
+
+
+def test_score_topk_argument_checks(env):
+    torch, L, lib, plan, rec = env
+    out = torch.empty((plan.n_seg, plan.k), dtype=torch.int64, device="cuda")
+    args = dict(archs=L.ptr(plan.h_archs), n_arch=plan.n_arch, rec=L.ptr(rec), n=plan.total,
+                base=0, mode=0, vtab=L.ptr(plan.d_vtab), n_var=plan.n_var, n_seg=plan.n_seg,
+                k=plan.k, ws=L.ptr(plan.d_ws), ws_bytes=plan.ws_bytes, out=L.ptr(out))
+
+    def call(**kw):
+        a = {**args, **kw}
+        return lib.occx_score_topk(L.ctx(), a["archs"], a["n_arch"], a["rec"], a["n"], a["base"],
+                                   a["mode"], a["vtab"], a["n_var"], a["n_seg"], a["k"], a["ws"],
+                                   a["ws_bytes"], a["out"], L.stream_ptr())
+    assert call() == 0
+    assert call(k=0) == 1 and call(k=33) == 1          # OCCX_ERR_VALUE
+    assert call(mode=2) == 1
+    assert call(ws_bytes=8) == 1                        # workspace too small
+    assert call(base=(1 << 34) - 2) == 8                # index space above 2^34: CAPACITY
+    assert call(n_arch=0) != 0
+
+
+def test_score_space_key_offset_capacity(env):
+    torch, L, lib, plan, rec = env
+    with pytest.raises(Exception):
+        plan.score_implicit(0, plan.total, key_offset=(1 << 34) - plan.total + 1)
+    a = plan.score_implicit(0, plan.total, key_offset=(1 << 34) - plan.total).cpu().numpy()
+    b = plan.score(rec, plan.total, index_base=(1 << 34) - plan.total).cpu().numpy()
+    assert np.array_equal(a, b)
+
+
+def test_mix_reduce_argument_checks(env):
+    torch, L, lib, plan, rec = env
+    buf = torch.zeros(64, dtype=torch.uint8, device="cuda")
+    off = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    lut = torch.zeros(4, dtype=torch.uint8, device="cuda")
+    out = torch.zeros(144, dtype=torch.uint8, device="cuda")
+    s = L.stream_ptr()
+    assert lib.occx_mix_reduce(L.ctx(), L.ptr(buf), L.ptr(off), 1, L.ptr(lut), 0, L.ptr(out), s) == 1
+    assert lib.occx_mix_reduce(L.ctx(), L.ptr(buf), L.ptr(off), 1, L.ptr(lut), 70000,
+                               L.ptr(out), s) == 1
+    assert lib.occx_mix_reduce(L.ctx(), L.ptr(buf) + 2, L.ptr(off), 1, L.ptr(lut), 4,
+                               L.ptr(out), s) == 1      # records must be 4-byte aligned
+    assert lib.occx_mix_reduce(L.ctx(), L.ptr(buf), L.ptr(off), 0, L.ptr(lut), 4, L.ptr(out), s) == 0
+
+
+def test_python_layer_maps_statuses(env):
+    from paper_1701_08547_b200 import (IllegalLaunchError, KernelResources,
+                                       UnsupportedArchitectureError, cost_estimate,
+                                       occupancy_batch, suggest_batch, workloads)
+    from paper_1701_08547_b200.mix import InstructionMix, OpClass
+    k20 = workloads.all_archs()[1]
+    ob = occupancy_batch(k20, [(0, 0, 0), (2048, 0, 0), (128, 27, 0)])
+    with pytest.raises(IllegalLaunchError):
+        ob.result(0)
+    with pytest.raises(IllegalLaunchError):
+        ob.result(1)
+    assert ob.result(2).active_blocks == 16
+    with pytest.raises(IllegalLaunchError):
+        suggest_batch([(k20, KernelResources("k", 300))])
+    with pytest.raises(UnsupportedArchitectureError):
+        cost_estimate(InstructionMix({OpClass.FP32: 3}, 0), 10.0)
+    with pytest.raises(ValueError):
+        cost_estimate(InstructionMix({OpClass.FP32: 3}, 0), 3.5, scale=0.0)
