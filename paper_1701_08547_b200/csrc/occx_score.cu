@@ -454,7 +454,7 @@ __device__ __forceinline__ uint4 ig_record(const IgCache& c, const uint32_t* poo
   return make_uint4(c.x, S, c.z, min(R, 0xffffu) | c.w_hi);
 }
 
-constexpr int kIgThreads = 512;                 // 16 warps, one CTA per SM (<= 128 registers)
+constexpr int kIgThreads = 768;                 // 24 warps per SM: 0.83 ms vs 0.94 (16) and 0.92 (32) on config 5
 constexpr int kIgWarps = kIgThreads / 32;
 constexpr int kIgTab = 1024;                    // per-warp separable-table words (|REGS| + |SMEM|)
 
