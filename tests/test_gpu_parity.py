@@ -239,6 +239,26 @@ def test_k2_config5_golden(P, torch, golden):
     assert keys.tolist() == g["corrected"]
 
 
+def test_config5_verbatim_full_size_vs_c_oracle(P, torch):
+    """Config 5 (1.28e9 candidates) in VERBATIM mode -- the reference's
+    unclamped register / shared-memory limits -- record path (K2) and
+    implicit grid (K2i, with a weak-scaling key offset) against the C oracle
+    over the whole space."""
+    import os
+    from paper_1701_08547_b200 import workloads
+    cfg = workloads.config5()
+    plan, keys = _score_config(P, torch, cfg, "verbatim", chunk=1 << 29)
+    want = oracle.score_spaces(problem_of(cfg, True), spaces_of(cfg),
+                               threads=max(2, len(os.sched_getaffinity(0))))
+    assert np.array_equal(keys, want)
+    off = 3 * plan.total
+    imp = plan.score_implicit(key_offset=off).cpu().numpy().view(np.uint64)
+    idx = (1 << 34) - 1 - (want & np.uint64((1 << 34) - 1))
+    shifted = np.where(want != 0, (want & ~np.uint64((1 << 34) - 1)) |
+                       (np.uint64((1 << 34) - 1) - (idx + np.uint64(off))), 0)
+    assert np.array_equal(imp, shifted)
+
+
 def test_k2_config1_decode(P, torch):
     from paper_1701_08547_b200 import workloads
     res = P.score_space(workloads.config1().kernels, workloads.config1().archs)
