@@ -184,6 +184,44 @@ def cpu_oracle_c(workload: str, mode: str, seconds_hint: float = 3.0):
 # secondary lines (rank 0, N = 1): config 3 (K0) and the implicit-grid API
 # ---------------------------------------------------------------------------
 
+def _cpu_aggregate_worker(args):
+    """oracle/pyref.aggregate (mix.py:245-261 restated: classify() per
+    instruction, guard rule, register operands) over kernels [k0, k1)."""
+    k0, k1 = args
+    from oracle import pyref
+    from paper_1701_08547_b200 import workloads
+    from paper_1701_08547_b200.mix import DEFAULT_OPCLASSES
+    c = workloads.make_corpus(k1 - k0, first=k0)
+    ops = workloads.corpus_opcodes()
+    table = {k: v.value for k, v in DEFAULT_OPCLASSES.items()}
+    regs = workloads._REGS_OF_TEMPLATE[c.ops].sum(axis=1)
+    instrs = [(ops[o], workloads.MOD_SUBSETS[s], g > 0, int(r))
+              for o, s, g, r in zip(c.opcode, c.subset, c.guard, regs)]
+    t0 = time.perf_counter()
+    for k in range(c.n_kernels):
+        pyref.aggregate(instrs[int(c.offsets[k]):int(c.offsets[k + 1])], table)
+    return time.perf_counter() - t0, c.n_instr
+
+
+def cpu_aggregate_baseline(n_kernels: int = 16000):
+    """Config-3 CPU path: the Python restatement of aggregate() on a sample of
+    the corpus, all host cores (one process per core, disjoint kernels)."""
+    import multiprocessing as mp
+    procs = len(os.sched_getaffinity(0))
+    per = max(1, n_kernels // procs)
+    chunks = [(i * per, (i + 1) * per) for i in range(procs)]
+    with mp.get_context("fork").Pool(procs) as pool:
+        t0 = time.perf_counter()
+        res = pool.map(_cpu_aggregate_worker, chunks)
+        wall = time.perf_counter() - t0
+    n = sum(r[1] for r in res)
+    busy = max(r[0] for r in res)
+    return {"value": n / busy, "unit": "instructions/s", "cores": procs, "kind": "port",
+            "sample": f"{per * procs} corpus kernels, {n} instructions; oracle/pyref.aggregate "
+                      f"(Python {sys.version.split()[0]}), {procs} processes, {busy:.2f} s "
+                      f"(wall {wall:.2f} s incl. input decode)"}
+
+
 def secondary_config3(hbm_peak: float):
     """K0 over the 100k-kernel corpus (config 3): instructions/s and HBM
     roofline (4 B/instruction + 8 B offset + 144 B output per kernel)."""
@@ -216,7 +254,8 @@ def secondary_config3(hbm_peak: float):
             "ms": ms, "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak,
                                    "unit": "GB/s", "frac": gbs / hbm_peak,
                                    "algorithmic_bytes": byts},
-            "l2": "512 MB buffer written between launches (flush)"}
+            "l2": "512 MB buffer written between launches (flush)",
+            "cpu_baseline": cpu_aggregate_baseline()}
 
 
 def secondary_space_api(cfg, mode: str, steps: int = 10):
