@@ -258,6 +258,32 @@ def secondary_config3(hbm_peak: float):
             "cpu_baseline": cpu_aggregate_baseline()}
 
 
+def secondary_records(name: str, mode: str, hbm_peak: float, steps: int = 20):
+    """K2 + K3 on another BASELINE config (inputs resident, > L2 for config 4;
+    config 2's 419 MB also exceeds the 126 MB L2)."""
+    import torch
+    from paper_1701_08547_b200 import ScorePlan, workloads
+    cfg = workloads.CONFIGS[name]()
+    plan = ScorePlan(cfg.kernels, cfg.archs, mode, k=cfg.k)
+    rec = plan.generate()
+    for _ in range(3):
+        plan.score(rec, plan.total)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        plan.score(rec, plan.total)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    gbs = 16 * plan.total / (ms / 1e3) / 1e9
+    return {"workload": cfg.name, "candidates": plan.total, "ms": ms,
+            "value": plan.total / (ms / 1e3), "unit": UNIT,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": gbs / hbm_peak}}
+
+
 def secondary_space_api(cfg, mode: str, steps: int = 10):
     """K2i, the kernel under score_space() (the e2e path): candidates decoded
     from their index, separable per-block limit tables.  No
@@ -501,7 +527,9 @@ def main():
     if rank == 0 and world == 1 and not args.no_secondary:
         secondary = {}
         for name, fn in (("config3_mix_reduce", lambda: secondary_config3(hbm_peak)),
-                         ("implicit_grid_score_space", lambda: secondary_space_api(cfg, args.mode))):
+                         ("implicit_grid_score_space", lambda: secondary_space_api(cfg, args.mode)),
+                         ("config4_records", lambda: secondary_records("config4", args.mode, hbm_peak)),
+                         ("config2_records", lambda: secondary_records("config2", args.mode, hbm_peak))):
             try:
                 secondary[name] = fn()
             except Exception as exc:
