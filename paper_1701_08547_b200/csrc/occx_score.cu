@@ -700,10 +700,18 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
 // ---- TMA feed ---------------------------------------------------------------
 constexpr int kTmaConsumerWarps = 16;
 constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
-constexpr int kTmaTile = 2048;                  // records per stage (32 KB)
-constexpr int kTmaStages = 4;
-static_assert(kTmaTile == kTmaConsumerWarps * 128, "4 records per consumer thread");
-constexpr size_t kTmaRingBytes = (size_t)kTmaStages * kTmaTile * 16;
+// Ring geometry by SL = contiguous 128-record slices per consumer warp per
+// tile: SL = 1: 4 stages of 2,048 records (32 KB); SL = 2: 3 stages of 4,096
+// (64 KB) -- each warp then sees 256 consecutive records per tile, halving
+// its (T, variant, arch) cache refills; used for large calls (config 5:
+// 3.11 -> 3.01 ms) where the deeper tiles' fill / drain cost is amortised.
+template <int SL> struct TmaRing {
+  static constexpr int kTile = 2048 * SL;
+  static constexpr int kStages = SL == 1 ? 4 : 3;
+  static constexpr size_t kBytes = (size_t)kStages * kTile * 16;
+};
+constexpr int kTmaTile = TmaRing<1>::kTile;     // chunk granularity (multiple of both tiles)
+constexpr uint64_t kTmaBigCall = 1ull << 28;    // candidates per call above which SL = 2
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -737,8 +745,12 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       : "memory");
 }
 
-template <int MODE, bool VT_SMEM>
+template <int MODE, bool VT_SMEM, int SL>
 __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __grid_constant__ ScoreParams p) {
+  constexpr int kTmaSlices = SL;
+  constexpr int kTmaTile = TmaRing<SL>::kTile;
+  constexpr int kTmaStages = TmaRing<SL>::kStages;
+  constexpr size_t kTmaRingBytes = TmaRing<SL>::kBytes;
   extern __shared__ __align__(128) unsigned char smem[];
   uint4* ring = reinterpret_cast<uint4*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTmaRingBytes);
@@ -782,21 +794,30 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
       const uint32_t cnt = (uint32_t)min((uint64_t)kTmaTile, end - tb);
       mbar_wait(&full[st], (t / kTmaStages) & 1u);
       const uint4* tile = ring + (size_t)st * kTmaTile;
-      const uint32_t slice = (uint32_t)(warp - 1) * 128u + lane;
-      uint4 r[4];
+      // warp w takes kTmaSlices contiguous 128-record slices of the tile, so
+      // its (T, variant, arch) cache sees kTmaSlices x 128 consecutive records
+      const uint32_t slice = (uint32_t)(warp - 1) * (128u * kTmaSlices) + lane;
+      uint4 r[kTmaSlices][4];
       if (cnt == (uint32_t)kTmaTile) {                // every tile but the last
 #pragma unroll
-        for (int j = 0; j < 4; ++j) r[j] = tile[slice + 32u * j];
+        for (int h = 0; h < kTmaSlices; ++h)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) r[h][j] = tile[slice + 128u * h + 32u * j];
       } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t idx = slice + 32u * j;
-          r[j] = idx < cnt ? tile[idx] : make_uint4(0, 0, 0, 0xffffffffu);
-        }
+        for (int h = 0; h < kTmaSlices; ++h)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t idx = slice + 128u * h + 32u * j;
+            r[h][j] = idx < cnt ? tile[idx] : make_uint4(0, 0, 0, 0xffffffffu);
+          }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);      // records are in registers
-      k2_process4<MODE, VT_SMEM>(s, cc, wl, r, kIdxMask - p.index_base - tb - slice, lane, p.k);
+#pragma unroll
+      for (int h = 0; h < kTmaSlices; ++h)
+        k2_process4<MODE, VT_SMEM>(s, cc, wl, r[h], kIdxMask - p.index_base - tb - slice - 128u * h,
+                                   lane, p.k);
     }
     k2_stage(wl, lane, p.k, stage, warp - 1);
   }
@@ -1158,13 +1179,19 @@ extern "C" int occx_score_topk(const occx_ctx* ctx, const occx_arch_t* h_archs, 
   p.partials = static_cast<uint64_t*>(d_ws);
   const int grid = score_grid(ctx);
   const int feed = score_feed();
-  const uint64_t tile = feed == kFeedTma ? (uint64_t)kTmaTile : (uint64_t)kLdgThreads * kLdgUnroll;
+  p.vt_smem = ((uint64_t)n_var * n_arch <= (uint64_t)kVtSmemMax) ? 1u : 0u;
+  size_t smem = k2_tail_bytes(p.archs, n_var, n_seg, k, p.vt_smem != 0);
+  // two slices per warp for big calls when the deeper ring fits
+  int sl = (feed == kFeedTma && n >= kTmaBigCall &&
+            smem + TmaRing<2>::kBytes + 2 * TmaRing<2>::kStages * 8 <= (size_t)ctx->max_smem_optin)
+               ? 2 : 1;
+  if (feed == kFeedTma)
+    smem += sl == 2 ? TmaRing<2>::kBytes + 2 * TmaRing<2>::kStages * 8
+                    : TmaRing<1>::kBytes + 2 * TmaRing<1>::kStages * 8;
+  const uint64_t tile = feed == kFeedTma ? (uint64_t)kTmaTile * sl : (uint64_t)kLdgThreads * kLdgUnroll;
   const uint64_t tiles = (n + tile - 1) / tile;
   p.chunk = ((tiles + grid - 1) / grid) * tile;
   if (p.chunk == 0) p.chunk = tile;
-  p.vt_smem = ((uint64_t)n_var * n_arch <= (uint64_t)kVtSmemMax) ? 1u : 0u;
-  size_t smem = k2_tail_bytes(p.archs, n_var, n_seg, k, p.vt_smem != 0);
-  if (feed == kFeedTma) smem += kTmaRingBytes + 2 * kTmaStages * 8;
   if (smem > (size_t)ctx->max_smem_optin) {
     if (!p.vt_smem) return OCCX_ERR_CAPACITY;
     p.vt_smem = 0;
@@ -1178,13 +1205,21 @@ extern "C" int occx_score_topk(const occx_ctx* ctx, const occx_arch_t* h_archs, 
     KERNEL<<<grid, THREADS, smem, s>>>(p);                                           \
   } while (0)
   const bool vts = p.vt_smem != 0;
-  if (feed == kFeedTma) {
+  if (feed == kFeedTma && sl == 2) {
     if (mode == OCCX_MODE_CORRECTED) {
-      if (vts) OCCX_LAUNCH_K2((score_topk_tma_kernel<0, true>), kTmaThreads);
-      else OCCX_LAUNCH_K2((score_topk_tma_kernel<0, false>), kTmaThreads);
+      if (vts) OCCX_LAUNCH_K2((score_topk_tma_kernel<0, true, 2>), kTmaThreads);
+      else OCCX_LAUNCH_K2((score_topk_tma_kernel<0, false, 2>), kTmaThreads);
     } else {
-      if (vts) OCCX_LAUNCH_K2((score_topk_tma_kernel<1, true>), kTmaThreads);
-      else OCCX_LAUNCH_K2((score_topk_tma_kernel<1, false>), kTmaThreads);
+      if (vts) OCCX_LAUNCH_K2((score_topk_tma_kernel<1, true, 2>), kTmaThreads);
+      else OCCX_LAUNCH_K2((score_topk_tma_kernel<1, false, 2>), kTmaThreads);
+    }
+  } else if (feed == kFeedTma) {
+    if (mode == OCCX_MODE_CORRECTED) {
+      if (vts) OCCX_LAUNCH_K2((score_topk_tma_kernel<0, true, 1>), kTmaThreads);
+      else OCCX_LAUNCH_K2((score_topk_tma_kernel<0, false, 1>), kTmaThreads);
+    } else {
+      if (vts) OCCX_LAUNCH_K2((score_topk_tma_kernel<1, true, 1>), kTmaThreads);
+      else OCCX_LAUNCH_K2((score_topk_tma_kernel<1, false, 1>), kTmaThreads);
     }
   } else {
     if (mode == OCCX_MODE_CORRECTED) {
