@@ -23,10 +23,10 @@ import numpy as np
 from . import _lib
 from .arch import ArchSpec, COST_KEY_OF_MAJOR, pack_archs
 from .errors import DeviceError, IllegalLaunchError
-from .mix import (CATEGORY_OF, COUNTABLE, CPI_ROW, DEFAULT_OPCLASSES, DEFAULT_THROUGHPUT,
+from .mix import (COUNTABLE, CPI_ROW, DEFAULT_OPCLASSES, DEFAULT_THROUGHPUT,
                   DEVICE_ID, Category, InstructionMix, OpClass, ThroughputTable,
                   classify_signature)
-from .occupancy import (LIMITER_OF_CODE, MODE_CODE, LaunchInput, Mode, OccupancyResult,
+from .occupancy import (LIMITER_OF_CODE, MODE_CODE, Mode, OccupancyResult,
                         SuggestionReport, thread_candidates)
 from .resources import register_operand_count
 from .tuning import TuningSpace, grid_size, membership_masks

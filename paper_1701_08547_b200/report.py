@@ -36,7 +36,7 @@ from .arch import ArchSpec
 from .batch import (FeatureBatch, SignatureTable, _to_device, _to_host, cost_key_of_cc,
                     feature_records, mix_from_record, mix_reduce, occupancy_batch,
                     pack_instructions, suggest_batch)
-from .mix import (DEFAULT_OPCLASSES, DEFAULT_THROUGHPUT, Category, InstructionMix, OpClass,
+from .mix import (DEFAULT_OPCLASSES, DEFAULT_THROUGHPUT, InstructionMix, OpClass,
                   category_cycles, per_class_cycles, pipeline_utilization)
 from .occupancy import Mode, OccupancyResult, SuggestionReport
 from .resources import KernelResources, parse_resource_report
@@ -300,4 +300,4 @@ def to_json(report: dict) -> str:
 
 __all__ = ["KernelAnalysis", "analyze_kernel", "analyze_batch", "analyze_listing",
            "resources_dict", "mix_dict", "occupancy_dict", "suggestion_dict", "prune_dict",
-           "kernel_dict", "report_dict", "to_json", "REPORT_FORMAT_VERSION", "Category"]
+           "kernel_dict", "report_dict", "to_json", "REPORT_FORMAT_VERSION"]

@@ -1,4 +1,4 @@
-import sys, time, numpy as np, torch
+import sys, time, torch
 sys.path.insert(0, '.')
 from paper_1701_08547_b200 import ScorePlan, workloads
 for name in ("config4", "config5"):

@@ -4,7 +4,6 @@ compute is attempted here)."""
 
 import ctypes
 
-import numpy as np
 import pytest
 
 from paper_1701_08547_b200 import _lib, workloads

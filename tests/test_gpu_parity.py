@@ -2,7 +2,6 @@
 the oracle, through the C ABI (ctypes).  Run on a B200: pytest -m gpu."""
 
 import hashlib
-import math
 
 import numpy as np
 import pytest

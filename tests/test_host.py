@@ -8,12 +8,12 @@ import numpy as np
 import pytest
 
 from oracle import pyref
-from paper_1701_08547_b200 import (ArchSpecError, Family, NoCandidatesError, ParseError,
+from paper_1701_08547_b200 import (ArchSpecError, NoCandidatesError, ParseError,
                                    PruneRule, TuningSpace, UnknownArchitectureError,
                                    builtin_arch, enumerate_space, grid_size, parse_space_file,
                                    resolve_arch, rule_prune, static_prune, thread_candidates)
 from paper_1701_08547_b200.arch import parse_arch_config, pack_archs
-from paper_1701_08547_b200.batch import (KernelSpec, decode_key, pack_launches, pack_mixes,
+from paper_1701_08547_b200.batch import (decode_key, pack_launches, pack_mixes,
                                          SignatureTable, mix_from_record)
 from paper_1701_08547_b200.mix import (DEFAULT_OPCLASSES, DEFAULT_THROUGHPUT, InstructionMix,
                                        OpClass, classify_signature, cpi, parse_opclass_table,

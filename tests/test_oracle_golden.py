@@ -4,7 +4,6 @@ Every fixture in tests/golden/ was produced by tests/golden/make_golden.py
 calling the reference occmix package itself.  CPU only.
 """
 
-import math
 
 import numpy as np
 import pytest

@@ -4,7 +4,6 @@ were recorded from the reference (tests/golden/make_golden.py `sass`), and
 the config-3 corpus.  CPU only -- the tokenizer is host code."""
 
 import numpy as np
-import pytest
 
 import oracle
 from helpers import load_golden
