@@ -519,15 +519,15 @@ __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
-// Fill TR[0, nR] and TS[0, nS + 3) (tr = the warp's table, shared address)
-// for the block ic points at; TR[nR] = 0 and TS[nS + t] = TS[t] pad the
-// +1-step lookups.  False (tables untouched) when they do not fit.
+// Fill TR[0, nR] and TS[0, nS + 7) (tr = the warp's table, shared address)
+// for the block ic points at; TR[nR] = 0 and TS[nS + t] = TS[t mod nS] pad
+// the +j lookups.  False (tables untouched) when they do not fit.
 template <int MODE, bool VT_SMEM>
 __device__ __forceinline__ bool sep_build(const SpaceParams& q, const K2Shared& s,
                                           const uint32_t* pool, const IgCache& ic,
                                           uint32_t tr, SepBlock& sb, int lane) {
   const uint32_t ns = ic.n_s, nr = ic.blk_n / ic.n_s;
-  if (nr + ns + 4 > q.sep_words) return false;
+  if (nr + ns + 8 > q.sep_words) return false;
   K2Cache kc;
   const uint4 r0 = make_uint4(ic.x, 0u, ic.z, ic.w_hi);       // R, S irrelevant here
   k2_fill<VT_SMEM>(s.c, r0, kc);
@@ -543,8 +543,8 @@ __device__ __forceinline__ bool sep_build(const SpaceParams& q, const K2Shared& 
     sts_u32(tr + 4u * i, ok ? (hi | (aw << 22)) : 0u);
   }
   if (lane == 0) sts_u32(tr + 4u * nr, 0u);
-  for (uint32_t i = (uint32_t)lane; i < ns + 3; i += 32) {
-    const uint32_t S = pool[ic.s_off + (i < ns ? i : i - ns)];
+  for (uint32_t i = (uint32_t)lane; i < ns + 7; i += 32) {
+    const uint32_t S = pool[ic.s_off + i % ns];
     const uint32_t aw = min(sep_ls<MODE>(arch, S) * wpb, wmp);
     sts_u32(tr + 4u * (nr + 1 + i), ok ? (hi | (aw << 22)) : 0u);
   }
@@ -639,6 +639,39 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
       ++ri;
     }
   };
+  // Two slices at `pb` as one: lane l takes candidates pb + 8l + j (j < 8),
+  // (ri, si) by one division; at most one REGS step when |SMEM| >= 8.
+  auto fast_pair = [&](uint64_t pb) {
+    const uint32_t o8 = (uint32_t)(pb - sb.lo) + 8u * (uint32_t)lane;
+    uint32_t v[8];
+    if (sb.ns >= 8) {
+      const uint32_t r0 = fastdiv(o8, sb.ds), s0 = o8 - r0 * sb.ns;
+      const uint32_t t0 = lds_u32(tr + 4u * r0), t1 = lds_u32(tr + 4u * r0 + 4u);
+      const uint32_t sa = sb.ts + 4u * s0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = min(s0 + j < sb.ns ? t0 : t1, lds_u32(sa + 4u * j));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t rj = fastdiv(o8 + j, sb.ds), sj = o8 + j - rj * sb.ns;
+        v[j] = min(lds_u32(tr + 4u * rj), lds_u32(sb.ts + 4u * sj));
+      }
+    }
+    const uint64_t inv0 = kIdxMask - q.key_off - (pb + 8u * (uint32_t)lane);
+    const uint32_t m = max(max(max(v[0], v[1]), max(v[2], v[3])),
+                           max(max(v[4], v[5]), max(v[6], v[7])));
+    const bool any = (m & 0x1fc00000u) &&
+                     (sb.seg != wl.seg || (m | (uint32_t)(inv0 >> 32)) > (uint32_t)(wl.thr >> 32));
+    if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint64_t inv = inv0 - (uint64_t)j;
+        const uint64_t key = (v[j] & 0x1fc00000u)
+            ? (((uint64_t)(v[j] | (uint32_t)(inv >> 32)) << 32) | (uint32_t)inv) : 0ull;
+        wl_offer(key, key ? sb.seg : wl.seg, wl, lane, p.k, s.thr, s.list, s.lock);
+      }
+    }
+  };
   for (uint64_t base = wb; base < we; base += 128) {
     if (base + 128 <= we) {
       ig_seek(q, pool, base, ic);                          // same g on every lane
@@ -646,17 +679,14 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
           sep_build<MODE, VT_SMEM>(q, s, pool, ic, tr, sb, lane)) {
         const uint64_t lb = (sb.lo + sb.n - base) >> 7, lr = (we - base) >> 7;
         left = (uint32_t)(lb < lr ? lb : lr);
-        o = (uint32_t)(base - sb.lo) + 4u * (uint32_t)lane;
-        ri = fastdiv(o, sb.ds);
-        si = o - ri * sb.ns;
-        dq = 128u / sb.ns;
-        dr = 128u - dq * sb.ns;
         // tight loop over the block's whole slices, two per trip
-        for (; left >= 2; left -= 2, base += 256) {
-          fast_slice(base);
-          fast_slice(base + 128);
-        }
-        if (left) {
+        for (; left >= 2; left -= 2, base += 256) fast_pair(base);
+        if (left) {                                        // an odd last slice
+          o = (uint32_t)(base - sb.lo) + 4u * (uint32_t)lane;
+          ri = fastdiv(o, sb.ds);
+          si = o - ri * sb.ns;
+          dq = 128u / sb.ns;
+          dr = 128u - dq * sb.ns;
           fast_slice(base);
           left = 0;
           base += 128;
