@@ -527,7 +527,7 @@ __device__ __forceinline__ bool sep_build(const SpaceParams& q, const K2Shared& 
                                           const uint32_t* pool, const IgCache& ic,
                                           uint32_t tr, SepBlock& sb, int lane) {
   const uint32_t ns = ic.n_s, nr = ic.blk_n / ic.n_s;
-  if (nr + ns + 8 > q.sep_words) return false;
+  if (nr + ns + 16 > q.sep_words) return false;
   K2Cache kc;
   const uint4 r0 = make_uint4(ic.x, 0u, ic.z, ic.w_hi);       // R, S irrelevant here
   k2_fill<VT_SMEM>(s.c, r0, kc);
@@ -543,7 +543,7 @@ __device__ __forceinline__ bool sep_build(const SpaceParams& q, const K2Shared& 
     sts_u32(tr + 4u * i, ok ? (hi | (aw << 22)) : 0u);
   }
   if (lane == 0) sts_u32(tr + 4u * nr, 0u);
-  for (uint32_t i = (uint32_t)lane; i < ns + 7; i += 32) {
+  for (uint32_t i = (uint32_t)lane; i < ns + 15; i += 32) {
     const uint32_t S = pool[ic.s_off + i % ns];
     const uint32_t aw = min(sep_ls<MODE>(arch, S) * wpb, wmp);
     sts_u32(tr + 4u * (nr + 1 + i), ok ? (hi | (aw << 22)) : 0u);
@@ -672,6 +672,38 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
       }
     }
   };
+  auto fast_quad = [&](uint64_t pb) {
+    const uint32_t o8 = (uint32_t)(pb - sb.lo) + 16u * (uint32_t)lane;
+    uint32_t v[16];
+    if (sb.ns >= 16) {
+      const uint32_t r0 = fastdiv(o8, sb.ds), s0 = o8 - r0 * sb.ns;
+      const uint32_t t0 = lds_u32(tr + 4u * r0), t1 = lds_u32(tr + 4u * r0 + 4u);
+      const uint32_t sa = sb.ts + 4u * s0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = min(s0 + j < sb.ns ? t0 : t1, lds_u32(sa + 4u * j));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t rj = fastdiv(o8 + j, sb.ds), sj = o8 + j - rj * sb.ns;
+        v[j] = min(lds_u32(tr + 4u * rj), lds_u32(sb.ts + 4u * sj));
+      }
+    }
+    const uint64_t inv0 = kIdxMask - q.key_off - (pb + 16u * (uint32_t)lane);
+    uint32_t m = v[0];
+#pragma unroll
+    for (int j = 1; j < 16; ++j) m = max(m, v[j]);
+    const bool any = (m & 0x1fc00000u) &&
+                     (sb.seg != wl.seg || (m | (uint32_t)(inv0 >> 32)) > (uint32_t)(wl.thr >> 32));
+    if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint64_t inv = inv0 - (uint64_t)j;
+        const uint64_t key = (v[j] & 0x1fc00000u)
+            ? (((uint64_t)(v[j] | (uint32_t)(inv >> 32)) << 32) | (uint32_t)inv) : 0ull;
+        wl_offer(key, key ? sb.seg : wl.seg, wl, lane, p.k, s.thr, s.list, s.lock);
+      }
+    }
+  };
   for (uint64_t base = wb; base < we; base += 128) {
     if (base + 128 <= we) {
       ig_seek(q, pool, base, ic);                          // same g on every lane
@@ -680,6 +712,7 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
         const uint64_t lb = (sb.lo + sb.n - base) >> 7, lr = (we - base) >> 7;
         left = (uint32_t)(lb < lr ? lb : lr);
         // tight loop over the block's whole slices, two per trip
+        for (; left >= 4; left -= 4, base += 512) fast_quad(base);
         for (; left >= 2; left -= 2, base += 256) fast_pair(base);
         if (left) {                                        // an odd last slice
           o = (uint32_t)(base - sb.lo) + 4u * (uint32_t)lane;
