@@ -13,6 +13,7 @@ packing membership masks.
 from __future__ import annotations
 
 import enum
+import functools
 from dataclasses import dataclass
 
 from .arch import ArchSpec
@@ -82,10 +83,16 @@ class SuggestionReport:
 
 def thread_candidates(arch: ArchSpec) -> tuple[int, ...]:
     """Block sizes whose blocks tile the SM's warp budget exactly
-    (ref occupancy.py:198-211).  Arch-level table, not per-candidate work."""
-    ws, wmp, bmp = arch.warp_size, arch.max_warps_per_mp, arch.max_blocks_per_mp
+    (ref occupancy.py:198-211).  Arch-level table, not per-candidate work:
+    memoised on the four fields it reads."""
+    return _thread_candidates(arch.warp_size, arch.max_warps_per_mp, arch.max_blocks_per_mp,
+                              arch.max_threads_per_block)
+
+
+@functools.lru_cache(maxsize=256)
+def _thread_candidates(ws: int, wmp: int, bmp: int, tmax: int) -> tuple[int, ...]:
     keep = []
-    for wpb in range(1, arch.max_threads_per_block // ws + 1):
+    for wpb in range(1, tmax // ws + 1):
         b = min(bmp, wmp // wpb)
         if b >= 1 and b * wpb == wmp:
             keep.append(wpb * ws)
