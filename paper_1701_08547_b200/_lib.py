@@ -127,7 +127,7 @@ _ctx: dict[int, int] = {}
 def ctx(device: int | None = None) -> int:
     """Per-device context handle (created once, immutable)."""
     import torch
-    if not torch.cuda.is_available():
+    if not _ctx and not torch.cuda.is_available():
         raise DeviceError("no CUDA device: the occx backend runs on the GPU only")
     dev = torch.cuda.current_device() if device is None else device
     with _lock:

@@ -38,11 +38,18 @@ U32_MAX = 0xFFFFFFFF
 IDX_MASK = (1 << 34) - 1
 
 
+_TORCH = None
+
+
 def _torch():
-    import torch
-    if not torch.cuda.is_available():
-        raise DeviceError("no CUDA device: the occx backend runs on the GPU only")
-    return torch
+    """torch, once a CUDA device is known to exist (checked on first use)."""
+    global _TORCH
+    if _TORCH is None:
+        import torch
+        if not torch.cuda.is_available():
+            raise DeviceError("no CUDA device: the occx backend runs on the GPU only")
+        _TORCH = torch
+    return _TORCH
 
 
 def _to_device(arr: np.ndarray):
