@@ -284,6 +284,70 @@ def secondary_records(name: str, mode: str, hbm_peak: float, steps: int = 20):
                          "frac": gbs / hbm_peak}}
 
 
+def secondary_suggest(mode: str, n_kernels: int = 100_000, steps: int = 20):
+    """K4 (batched suggest()): Table VI outputs for a
+    100k-kernel corpus on the five config archs (500k requests; registers
+    0..80, shared memory 0..48 KB), device-level call, plus the Python
+    restatement (oracle/pyref.suggest) on a sample on all host cores."""
+    import multiprocessing as mp
+    import numpy as np
+    import torch
+    from paper_1701_08547_b200 import _lib, batch, workloads
+    from paper_1701_08547_b200.arch import pack_archs
+    from paper_1701_08547_b200.occupancy import MODE_CODE, Mode
+    archs = workloads.all_archs()
+    rng = np.random.default_rng(1701)
+    n = n_kernels * len(archs)
+    inp = np.zeros(n, _lib.SUGG_IN)
+    inp["arch"] = np.repeat(np.arange(len(archs)), n_kernels)
+    inp["regs"] = np.tile(rng.integers(0, 81, n_kernels), len(archs))
+    inp["smem"] = np.tile(rng.integers(0, 48, n_kernels) * 1024, len(archs))
+    h_archs = pack_archs(archs)
+    d_in, d_out = batch._to_device(inp), batch._empty(n * _lib.SUGG.itemsize)
+    lib, ctx = _lib.load(), _lib.ctx()
+
+    def run():
+        _lib.check(lib.occx_suggest_batch(ctx, _lib.ptr(h_archs), len(h_archs), _lib.ptr(d_in), n,
+                                          MODE_CODE[Mode(mode)], _lib.ptr(d_out),
+                                          _lib.stream_ptr()), "occx_suggest_batch")
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    procs = len(os.sched_getaffinity(0))
+    sample = [(int(a), int(r), int(s)) for a, r, s in inp[:: max(1, n // 200000)]
+              [["arch", "regs", "smem"]].tolist()]
+    with mp.get_context("fork").Pool(procs) as pool:
+        t0 = time.perf_counter()
+        pool.map(_cpu_suggest_worker, [(sample[i::procs], mode) for i in range(procs)])
+        wall = time.perf_counter() - t0
+    return {"kernel": "suggest_kernel (K4)", "requests": n, "ms": ms,
+            "value": n / (ms / 1e3), "unit": "suggestions/s",
+            "cpu_baseline": {"value": len(sample) / wall, "unit": "suggestions/s",
+                             "cores": procs, "kind": "port",
+                             "sample": f"{len(sample)} requests, oracle/pyref.suggest, "
+                                       f"{procs} processes, {wall:.2f} s"}}
+
+
+def _cpu_suggest_worker(args):
+    reqs, mode = args
+    from oracle import pyref
+    from paper_1701_08547_b200 import workloads
+    archs = workloads.all_archs()
+    for a, r, s in reqs:
+        try:
+            pyref.suggest(archs[a], r, s, verbatim=(mode == "verbatim"))
+        except pyref.OracleIllegalLaunch:
+            pass
+    return len(reqs)
+
+
 def secondary_space_api(cfg, mode: str, steps: int = 10):
     """K2i, the kernel under score_space() (the e2e path): candidates decoded
     from their index, separable per-block limit tables.  No
@@ -529,6 +593,7 @@ def main():
         for name, fn in (("config3_mix_reduce", lambda: secondary_config3(hbm_peak)),
                          ("implicit_grid_score_space", lambda: secondary_space_api(cfg, args.mode)),
                          ("config4_records", lambda: secondary_records("config4", args.mode, hbm_peak)),
+                         ("suggest_100k_kernels", lambda: secondary_suggest(args.mode)),
                          ("config2_records", lambda: secondary_records("config2", args.mode, hbm_peak))):
             try:
                 secondary[name] = fn()
