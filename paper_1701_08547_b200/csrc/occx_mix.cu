@@ -140,7 +140,7 @@ __device__ __forceinline__ void count_piece(MixAcc& a, const uint32_t (&lv)[8],
     const uint32_t l = lv[e];
     uint32_t dx, dy;
     if (e < kLdsRecords) {         // shared increment table: entry at byte 2 * l
-      const uint2 d = *reinterpret_cast<const uint2*>(incb + 2u * l);
+      const uint2 d = *reinterpret_cast<const uint2*>(incb + (l << 6));   // entry l/4, this lane's copy
       dx = d.x;
       dy = d.y;
     } else {                       // arithmetic: balances the shared-memory and ALU pipes
@@ -242,14 +242,14 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // Shared-memory layout: [64] u64 increments | [warps][32] first positions
 // (slots 0-16) and reduction scratch (24-31) | per-warp ring of kDepth chunks (kChunk records each) | class table.
 constexpr int kFirstStride = 32;                      // per warp: 17 first slots, 8-word scratch at 24
-__host__ __device__ constexpr size_t mix_ring_offset() { return 64 * 8 + kWarps * kFirstStride * 4; }
+__host__ __device__ constexpr size_t mix_ring_offset() { return 64 * 32 * 8 + kWarps * kFirstStride * 4; }
 
 template <int kDepth>
 __global__ void __launch_bounds__(kMixThreads, 1) mix_reduce_kernel(const __grid_constant__ MixParams p,
                                                                      uint32_t lut_mask) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* inc = reinterpret_cast<uint64_t*>(smem);
-  uint32_t* firsts = reinterpret_cast<uint32_t*>(inc + 64);
+  uint32_t* firsts = reinterpret_cast<uint32_t*>(inc + 64 * 32);
   uint4* ring = reinterpret_cast<uint4*>(smem + mix_ring_offset());
   unsigned char* lut = reinterpret_cast<unsigned char*>(ring + (size_t)kWarps * kDepth * (kChunk / 4));
   const int lane = threadIdx.x & 31;
@@ -269,9 +269,11 @@ __global__ void __launch_bounds__(kMixThreads, 1) mix_reduce_kernel(const __grid
   }
 
   // increment table indexed by class-table byte / 4 (= c + 32 * guard):
-  // entries 15..31 and 47..63 are zero (31 = the null entry)
-  for (uint32_t i = threadIdx.x; i < 64; i += blockDim.x) {
-    const uint32_t c = i & 31u, g = i >> 5;
+  // entries 15..31 and 47..63 are zero (31 = the null entry).  Replicated
+  // per lane ([entry][lane], 16 KB): lane l reads banks 2l, 2l+1 only, so an
+  // LDS.64 of 32 lanes is two conflict-free wavefronts whatever the classes.
+  for (uint32_t i = threadIdx.x; i < 64 * 32; i += blockDim.x) {
+    const uint32_t e = i >> 5, c = e & 31u, g = e >> 5;
     uint64_t v = 0;
     if (c < 15) {
       v = 1ull << (4 * c);
@@ -311,7 +313,7 @@ __global__ void __launch_bounds__(kMixThreads, 1) mix_reduce_kernel(const __grid
   }
   __syncthreads();
   if (ks >= ke) return;
-  const unsigned char* incb = reinterpret_cast<const unsigned char*>(inc);
+  const unsigned char* incb = reinterpret_cast<const unsigned char*>(inc) + 8 * lane;
   uint32_t* my_first = firsts + (threadIdx.x >> 5) * kFirstStride;
 
   // Positions are kept relative to the warp's first chunk start cs0 (u32:
