@@ -78,32 +78,51 @@ class ClockSampler:
         nv = self.nv
         while not self._stop.is_set():
             try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                t = time.perf_counter()
+                mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if r & bit:
-                        self.reasons.add(name)
+                self.samples.append((t, mhz, r))
             except Exception:
                 pass
-            time.sleep(0.002)
+            time.sleep(0.001)
 
-    def __enter__(self):
+    def start(self):
+        """Start polling early (the first NVML calls can be slow); only the
+        samples inside window_open()/window_close() are reported."""
         if self.ok:
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
+        self.w0 = self.w1 = None
         return self
 
-    def __exit__(self, *a):
+    def window_open(self):
+        self.w0 = time.perf_counter()
+
+    def window_close(self):
+        self.w1 = time.perf_counter()
+        if self.ok:
+            time.sleep(0.005)              # one more sample after the window
         self._stop.set()
         if self.ok:
             self._t.join()
 
     def summary(self):
-        if not self.ok or not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                    "samples": len(self.samples)}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+        inside = [s for s in self.samples if self.w0 is not None and self.w0 <= s[0] <= self.w1]
+        note = "inside the timed region"
+        if len(inside) < 3 and self.samples:   # short region: add the nearest samples around it
+            near = sorted(self.samples, key=lambda s: min(abs(s[0] - self.w0), abs(s[0] - self.w1)))
+            inside = sorted(set(inside) | set(near[:3]))
+            note = "timed region plus the nearest samples around it"
+        if not self.ok or not inside:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [],
+                    "samples": 0}
+        reasons = set()
+        for _, _, r in inside:
+            for bit, name in self.REASONS.items():
+                if r & bit:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(s[1] for s in inside), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons - {"gpu_idle"}), "samples": len(inside), "window": note}
 
 
 # ---------------------------------------------------------------------------
@@ -478,21 +497,22 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    sampler = ClockSampler(torch.cuda.current_device()).start()
     for _ in range(args.warmup):
         out = step()
     torch.cuda.synchronize()
     barrier()
-    sampler = ClockSampler(torch.cuda.current_device())
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with sampler:
-        torch.cuda.synchronize()
-        barrier()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            out = step()
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
+    torch.cuda.synchronize()
+    barrier()
+    sampler.window_open()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        out = step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    sampler.window_close()
+    barrier()
     ms_max = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     value = global_total / (ms_max / 1e3)
     final_keys = out.cpu().numpy().view(np.uint64)
