@@ -262,3 +262,35 @@ def test_random_big_blocks_k2i_vs_oracle(seed):
             r = plan.score(plan.generate(b, n), n, index_base=b + off).cpu().numpy()
             assert np.array_equal(a, r), (seed, mode, b, n, off)
         del rec
+
+
+@pytest.mark.parametrize("n_sig", [32_767, 40_000, 65_535])
+def test_k0_large_signature_tables(n_sig):
+    """Class tables above 64 KB switch K0 to its shallow ring (2 chunks in
+    flight); the 65,535-signature maximum of the record format included."""
+    import torch  # noqa: F401
+    rng = np.random.default_rng(n_sig)
+    lut = rng.integers(0, 15, n_sig).astype(np.uint8)
+    lens = rng.integers(0, 3000, 400)
+    lens[::37] = 0
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    n = int(off[-1])
+    sig = rng.integers(0, n_sig, n).astype(np.uint32)
+    rec = ((rng.random(n) < 0.15).astype(np.uint32) | (sig << 1) |
+           (rng.integers(0, 256, n).astype(np.uint32) << 17))
+    from paper_1701_08547_b200 import batch
+    out = _k0_run(batch._to_device(rec), off, lut)
+    _k0_check(out, rec, off, lut)
+
+
+@pytest.mark.parametrize("k", [1, 32])
+def test_k2_k2i_extreme_k(k):
+    import paper_1701_08547_b200 as P
+    rng = random.Random(77 + k)
+    cfg = random_big_block_config(rng, n_arch=2, n_kern=2)
+    cfg = type(cfg)(cfg.name, cfg.kernels, cfg.archs, k)
+    prob = oracle.problem_of(cfg)
+    want = oracle.score_spaces(prob, oracle.spaces_of(cfg), threads=4)
+    plan = P.ScorePlan(cfg.kernels, cfg.archs, k=k)
+    assert np.array_equal(plan.score(plan.generate(), plan.total).cpu().numpy().view(np.uint64), want)
+    assert np.array_equal(plan.score_implicit().cpu().numpy().view(np.uint64), want)
