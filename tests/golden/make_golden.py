@@ -15,6 +15,9 @@ with sys.version (CPython's float sum() changed in 3.12):
                          3000 random mixes (cost/intensity/shares as hex)
   corpus.json            aggregate() of the reference parser over the first
                          2000 kernels of the config-3 corpus text
+  specs.json             parse_space_file / parse_arch_config / parse_opclass_table
+                         outcomes (values or error class, line, message) on
+                         fuzzed spec texts
   topk_config{1,2,4}.json (and 5 with --big): per-segment top-16 keys of
                          the scoring composition, computed from reference
                          functions (limit tables, static/rule_prune,
@@ -488,6 +491,158 @@ def report_golden(n_kernels=120):
           len(out["corpus"]))
 
 
+# ---------------------------------------------------------------------------
+# spec-file parsers (space files, arch INI, opcode-class tables)
+# ---------------------------------------------------------------------------
+
+def _outcome(f, text, dump):
+    try:
+        return ["ok", dump(f(text))]
+    except R.StaticAnalysisError as exc:
+        return ["err", type(exc).__name__, getattr(exc, "line", None), str(exc)]
+    except Exception as exc:  # reference quirks (TypeError, raw ValueError, ...)
+        return ["err", type(exc).__name__, None, str(exc)]
+
+
+def _dump_space(sp):
+    return [[n, list(v)] for n, v in sp._dimensions()]
+
+
+def _dump_archs(specs):
+    import dataclasses
+    return [{k: (v.value if hasattr(v, "value") else v)
+             for k, v in dataclasses.asdict(s).items()} for s in specs]
+
+
+def _dump_opclasses(table):
+    return [[k, v.value] for k, v in table.items()]
+
+
+def _rand_space_text(rng):
+    names = ["TC", "BC", "UIF", "PL", "CFLAGS", "tc", "Cflags", "X", "N_2", "uif"]
+    ints = lambda: rng.choice([0, 1, 2, 5, 16, 24, 32, 48, 64, 96, 100, 192, 1025, -32, -1])
+
+    def rhs():
+        k = rng.randrange(9)
+        sp = lambda: rng.choice(["", " ", "  ", "\t"])
+        if k <= 2:
+            args = [str(ints()) for _ in range(rng.choice([2, 2, 3, 1, 4]))]
+            if rng.random() < 0.2:
+                args[-1] = "0"
+            return "range(" + sp() + (sp() + "," + sp()).join(args) + sp() + ")"
+        if k <= 5:
+            toks = []
+            for _ in range(rng.randrange(0, 5)):
+                toks.append(rng.choice([str(ints()), "'-use_fast_math'", "''", '"-O3"', "'",
+                                        '"', "x", "1.5", " 32 ", "'a", "0x20", "+64", "- 1"]))
+            return rng.choice(["[", "[ "]) + ",".join(toks) + rng.choice(["]", " ]"])
+        return rng.choice(["range(1,5", "[1,2", "{1,2}", "range(a,b)", "1", "", "range(1 , 5 , 2)",
+                           "[32, 64] extra", "range(-64,0,-32)"])
+
+    if rng.random() < 0.45:                          # well-formed file
+        lines = []
+        for name in rng.sample(names, rng.randrange(1, 5)):
+            if name.upper() == "TC":
+                vals = rng.choice(["range(32,1025,32)", "[64, 128,256]", "range(64, 513, 64)",
+                                   "[32]", "range(1024,0,-32)", "[96,32,96]"])
+            elif name.upper() == "CFLAGS":
+                vals = rng.choice(["['', '-use_fast_math']", '["-O3"]', "['a','b','c']"])
+            else:
+                vals = rng.choice(["range(1,6)", "[16, 48]", "range(24,193,24)", "[7]",
+                                   "range( 2 , 11 , 3 )", "['x', 2]"])
+            lines.append(f"param {name}[] = {vals};")
+        return rng.choice(_NL[:2]).join(lines)
+    lines = []
+    for _ in range(rng.randrange(0, 7)):
+        r = rng.random()
+        if r < 0.1:
+            lines.append(rng.choice(["", "   ", "# comment", "// note", "#param TC[] = [1];"]))
+        elif r < 0.17:
+            lines.append(rng.choice(["param TC = [32];", "parm TC[] = [32];", "param [] = [1];",
+                                     "param TC[ ] = [32, 64]", "param\tBC[]\t=\t[24];;",
+                                     "PARAM TC[] = [32];", "param TC[]=[32];  "]))
+        else:
+            lines.append(f"param {rng.choice(names)}[] = {rhs()}{rng.choice([';', ';', '', ' ;'])}")
+    return rng.choice(_NL[:2]).join(lines)
+
+
+def _rand_arch_text(rng):
+    base = [ln for ln in W.SM100_INI.splitlines() if "=" in ln]
+    sections = []
+    for si in range(rng.choice([1, 1, 1, 2, 0])):
+        body = list(base)
+        for _ in range(rng.randrange(0, 3)):
+            j = rng.randrange(len(body))
+            key = body[j].split("=")[0].strip()
+            op = rng.randrange(7)
+            if op == 0:
+                del body[j]
+            elif op == 1:
+                body[j] = f"{key} = {rng.choice(['abc', '1.5', '', '-4', '0', '10', '1e3', ' 7 '])}"
+            elif op == 2:
+                body.append(f"{rng.choice(['cuda_cores_per_mp', 'global_mem_mb', 'gpu_clock_mhz', 'mem_clock_mhz', 'constant_mem_bytes', 'l2_cache_mb', 'bogus_key'])}"
+                            f" = {rng.choice(['128', '40960', 'x', '1.5', '50'])}")
+            elif op == 3:
+                body[j] = f"{key} = {rng.choice(['31', '33', '64', '96', '1024', '2049', '4', '255'])}"
+            elif op == 4:
+                body.insert(j, rng.choice(["garbage line", "; comment", "# c", "  indented = 1",
+                                           "key: value", "= 3"]))
+            elif op == 5:
+                body[j] = "family = " + rng.choice(["KEPLER", "fermi", "volta", "other", ""])
+            else:
+                body.append(body[j])                               # duplicate option
+        name = rng.choice(["sm100-b200", "kepler", "my arch", "x", "sm100-b200"])
+        sections.append([f"[{name}]"] + body)
+    lines = [ln for sec in sections for ln in sec]
+    if rng.random() < 0.1:
+        lines.insert(0, rng.choice(["orphan = 1", "[broken", "[]"]))
+    return "\n".join(lines)
+
+
+def _rand_opclass_text(rng):
+    classes = [c.value for c in R.OpClass] + ["Bogus", "fp32", "Regs"]
+    keys = ["FFMA", "DADD", "F2F.F64", "I2F.U32", "LDG.E.64", "IMAD", "X1", "ffma", "1ABC",
+            "F2F .F64", "BRA", "MOV32I"]
+    lines = []
+    if rng.random() < 0.4:                           # well-formed table
+        for _ in range(rng.randrange(1, 12)):
+            lines.append(f"{rng.choice(keys[:8] + keys[10:])} -> "
+                         f"{rng.choice([c.value for c in R.OpClass if c is not R.OpClass.REGS])}")
+        return "\n".join(lines)
+    for _ in range(rng.randrange(0, 8)):
+        r = rng.random()
+        if r < 0.1:
+            lines.append(rng.choice(["", "# x", "  # y", "FFMA => FP32", "FFMA ->", "-> FP32"]))
+        else:
+            lines.append(f"{rng.choice(keys)}{rng.choice([' -> ', '->', '  ->\t', ' - > '])}"
+                         f"{rng.choice(classes)}{rng.choice(['', '', ' ', ' extra'])}")
+    return rng.choice(_NL[:2]).join(lines)
+
+
+def specs_golden(n=1500):
+    rng = random.Random(0x5BEC)
+    out = {"meta": META, "space": [], "arch": [], "opclass": []}
+    for _ in range(n):
+        t = _rand_space_text(rng)
+        out["space"].append({"text": t, "result": _outcome(R.parse_space_file, t, _dump_space)})
+    for _ in range(n // 3):
+        t = _rand_arch_text(rng)
+        out["arch"].append({"text": t, "result": _outcome(R.arch.parse_arch_config, t, _dump_archs)})
+    for _ in range(n // 3):
+        t = _rand_opclass_text(rng)
+        out["opclass"].append({"text": t, "result": _outcome(Rmix.parse_opclass_table, t,
+                                                             _dump_opclasses)})
+    for k in ("space", "arch", "opclass"):
+        kinds = {}
+        for c in out[k]:
+            key = c["result"][0] if c["result"][0] == "ok" else c["result"][1]
+            kinds[key] = kinds.get(key, 0) + 1
+        out["outcomes_" + k] = kinds
+        print(k, kinds)
+    with open(os.path.join(HERE, "specs.json"), "w") as fh:
+        json.dump(out, fh, ensure_ascii=True)
+
+
 if __name__ == "__main__":
     steps = sys.argv[1:] or ["tables", "random", "suggest", "mix", "corpus", "config1",
                              "config2", "config4"]
@@ -497,6 +652,6 @@ if __name__ == "__main__":
         t0 = time.time()
         {"tables": occupancy_tables, "random": occupancy_random, "suggest": suggest_golden,
          "mix": mix_golden, "corpus": corpus_golden, "sass": sass_golden,
-         "report": report_golden}.get(
+         "report": report_golden, "specs": specs_golden}.get(
             s, lambda: topk_golden(s))()
         print(f"{s}: {time.time() - t0:.1f}s", flush=True)
