@@ -25,6 +25,7 @@ the prunes; kernels in input order).
 
 from __future__ import annotations
 
+import enum
 import json
 import sys
 from dataclasses import dataclass, field
@@ -183,71 +184,62 @@ def analyze_listing(arch: ArchSpec, resource_report: str, disassembly: str,
 # ---------------------------------------------------------------------------
 
 def _number(x: float):
-    return "inf" if x == float("inf") else x
+    return "inf" if x == float("inf") else x       # JSON has no infinity literal
+
+
+def _plain(v):
+    """Enum -> its value, tuple/list -> list (recursively), else unchanged."""
+    if isinstance(v, enum.Enum):
+        return v.value
+    if isinstance(v, (tuple, list)):
+        return [_plain(x) for x in v]
+    return v
+
+
+def _record(obj, layout: str) -> dict:
+    """Project ``obj`` onto an ordered JSON object.  ``layout`` lists the
+    keys in output order; ``key=attr`` reads a differently named attribute."""
+    out = {}
+    for item in layout.split():
+        key, _, attr = item.partition("=")
+        out[key] = _plain(getattr(obj, attr or key))
+    return out
+
+
+# Field order of each object (ref report.py:89-151): part of the format.
+_RESOURCES = ("entry_name registers_per_thread static_shared_mem const_mem_banks "
+              "spill_loads spill_stores target_cc")
+_MIX_TOTALS = "flops mem ctrl reg_operands unclassified total_instructions"
+_OCCUPANCY = ("warps_per_block limit_warps limit_regs limit_smem active_blocks "
+              "active_warps occupancy limiter mode")
+_SUGGESTION = ("thread_candidates registers_used register_headroom smem_budget "
+               "best_occupancy best_threads best_blocks")
+_PRUNE = "rule=rule_applied original_size pruned_size reduction kept_thread_counts"
 
 
 def resources_dict(res: KernelResources) -> dict:
-    return {
-        "entry_name": res.entry_name,
-        "registers_per_thread": res.registers_per_thread,
-        "static_shared_mem": res.static_shared_mem,
-        "const_mem_banks": [[bank, size] for bank, size in res.const_mem_banks],
-        "spill_loads": res.spill_loads,
-        "spill_stores": res.spill_stores,
-        "target_cc": res.target_cc,
-    }
+    return _record(res, _RESOURCES)
 
 
 def mix_dict(mix: InstructionMix) -> dict:
-    counts = mix.counts
-    return {
-        "counts": {c.value: counts[c] for c in OpClass if counts.get(c)},
-        "flops": mix.flops,
-        "mem": mix.mem,
-        "ctrl": mix.ctrl,
-        "reg_operands": mix.reg_operands,
-        "unclassified": mix.unclassified,
-        "total_instructions": mix.total_instructions,
-    }
+    """Non-zero counts in OpClass order, then the category totals."""
+    present = {c.value: mix.counts[c] for c in OpClass if mix.counts.get(c)}
+    return {"counts": present, **_record(mix, _MIX_TOTALS)}
 
 
 def occupancy_dict(result: OccupancyResult) -> dict:
-    return {
-        "warps_per_block": result.warps_per_block,
-        "limit_warps": result.limit_warps,
-        "limit_regs": result.limit_regs,
-        "limit_smem": result.limit_smem,
-        "active_blocks": result.active_blocks,
-        "active_warps": result.active_warps,
-        "occupancy": result.occupancy,
-        "limiter": result.limiter.value,
-        "mode": result.mode.value,
-    }
+    return _record(result, _OCCUPANCY)
 
 
 def suggestion_dict(sugg: SuggestionReport) -> dict:
-    return {
-        "thread_candidates": list(sugg.thread_candidates),
-        "registers_used": sugg.registers_used,
-        "register_headroom": sugg.register_headroom,
-        "smem_budget": sugg.smem_budget,
-        "best_occupancy": sugg.best_occupancy,
-        "best_threads": sugg.best_threads,
-        "best_blocks": sugg.best_blocks,
-    }
+    return _record(sugg, _SUGGESTION)
 
 
 def prune_dict(report: PruneReport) -> dict:
-    d = {
-        "rule": report.rule_applied.value,
-        "original_size": report.original_size,
-        "pruned_size": report.pruned_size,
-        "reduction": report.reduction,
-        "kept_thread_counts": list(report.kept_thread_counts),
-    }
-    if report.intensity is not None:
-        d["intensity"] = _number(report.intensity)
-        d["intensity_source"] = report.intensity_source
+    d = _record(report, _PRUNE)
+    if report.intensity is not None:        # rule_prune reports only
+        d.update(intensity=_number(report.intensity),
+                 intensity_source=report.intensity_source)
     return d
 
 
