@@ -19,6 +19,16 @@ using namespace occx;
 
 namespace {
 
+#ifdef OCCX_K2_TIMING
+__device__ unsigned long long g_k2_cnt[8 * 1024];
+__device__ unsigned long long g_k2_hist[16 * 1024];
+#define K2_COUNT(i) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_k2_cnt[blockIdx.x * 8 + (i)], 1ull); } while (0)
+#define K2_ADD(i, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_k2_cnt[blockIdx.x * 8 + (i)], (unsigned long long)(v)); } while (0)
+__device__ __forceinline__ long long k2_clk() { long long c; asm volatile("mov.u64 %0, %%clock64;" : "=l"(c)); return c; }
+#else
+#define K2_COUNT(i) do { } while (0)
+#endif
+
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   uint4 v;
   asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -86,21 +96,62 @@ struct ScoreParams {
   uint64_t* partials;       // [gridDim.x][n_seg][k]
 };
 
+// Descending bitonic sort of one u64 per lane across the warp (lane 0 = largest).
+__device__ __forceinline__ uint64_t warp_sort_desc(uint64_t x, int lane) {
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const uint64_t o = __shfl_xor_sync(0xffffffffu, x, stride);
+      const bool keep_max = ((lane & stride) == 0) == ((lane & size) == 0);
+      x = keep_max ? (x > o ? x : o) : (x < o ? x : o);
+    }
+  }
+  return x;
+}
+
+// Many lanes beat a top-k list at once (a better thread count starts, a
+// fresh list, a whole warp list flushed into the CTA table): instead of up to
+// 32 dependent insertions, sort the batch and merge -- lane i < k takes
+// max(list[i], batch[k-1-i]), a bitonic sequence holding exactly the top k of
+// both (Batcher), then one bitonic merge.  Same result as inserting the keys
+// one at a time (keys are unique).  Lanes >= k come back 0.
+constexpr int kBatchMerge = 6;
+
+__device__ __noinline__ uint64_t list_merge_batch(uint64_t list, uint64_t x, int lane, uint32_t k) {
+  x = warp_sort_desc(x, lane);
+  const uint64_t xr = __shfl_sync(0xffffffffu, x, ((int)k - 1 - lane) & 31);
+  uint64_t y = lane < (int)k ? (list > xr ? list : xr) : 0ull;
+  if ((k & (k - 1)) == 0) {
+    for (uint32_t stride = k >> 1; stride > 0; stride >>= 1) {
+      const uint64_t o = __shfl_xor_sync(0xffffffffu, y, stride);
+      y = (lane & stride) == 0 ? (y > o ? y : o) : (y < o ? y : o);
+    }
+  } else {
+    y = warp_sort_desc(y, lane);
+  }
+  return y;
+}
+
 __device__ __forceinline__ void cta_insert(unsigned pend, uint64_t key, uint32_t seg,
                                            int lane, uint32_t k, volatile uint64_t* s_thr,
                                            volatile uint64_t* s_list, int* s_lock) {
   while (pend) {
+    K2_COUNT(4);
     const int src = __ffs(pend) - 1;
     const uint32_t sseg = __shfl_sync(0xffffffffu, seg, src);
     const unsigned same = pend & __ballot_sync(0xffffffffu, seg == sseg);
     if (lane == 0) {
-      while (atomicCAS(&s_lock[sseg], 0, 1) != 0) {
-      }
+      while (atomicCAS(&s_lock[sseg], 0, 1) != 0) __nanosleep(32);
       __threadfence_block();
     }
     __syncwarp();
     uint64_t mine = (lane < (int)k) ? s_list[sseg * k + lane] : 0ull;
     unsigned todo = same;
+    if (__popc(todo) >= kBatchMerge) {
+      mine = list_merge_batch(mine, (todo >> lane) & 1u ? key : 0ull, lane, k);
+      todo = 0;
+    }
     while (todo) {
       const int l = __ffs(todo) - 1;
       todo &= todo - 1;
@@ -123,22 +174,32 @@ __device__ __forceinline__ void cta_insert(unsigned pend, uint64_t key, uint32_t
 // Per-warp top-k list held in registers (lane j < k: j-th best key of the
 // warp's current segment).  Candidates are offered against the warp's own
 // exact threshold, so the common case costs one 64-bit compare and a ballot
-// and improvement bursts need no lock; the list is merged into the CTA's
-// shared table (under its lock) only when the warp moves to another segment
-// and at the end of the chunk.
+// and improvement bursts need no lock.  When the warp moves to another
+// segment its list becomes the warp's "previous" list (still in registers);
+// both are staged in shared memory at the end of the chunk and merged by one
+// warp.  Only a third segment in one chunk merges the previous list into the
+// CTA's shared table under its lock -- at a segment boundary all warps of
+// the CTA change segment within one tile, and taking the lock there was a
+// 16-warp convoy that made boundary CTAs up to 2x slower.
 constexpr uint32_t kNoSeg = 0xffffffffu;
 
 struct WarpList {
   uint64_t v;
   uint64_t thr;
   uint32_t seg;
+  uint32_t pseg;        // segment of the previous list (kNoSeg: none)
+  uint64_t pv;          // previous list, lane j < k
 };
 
 __device__ __forceinline__ void wl_flush(WarpList& w, int lane, uint32_t k, volatile uint64_t* s_thr,
                                          volatile uint64_t* s_list, int* s_lock) {
   if (w.seg != kNoSeg) {
-    const unsigned pend = __ballot_sync(0xffffffffu, lane < (int)k && w.v > s_thr[w.seg]);
-    if (pend) cta_insert(pend, w.v, w.seg, lane, k, s_thr, s_list, s_lock);
+    if (w.pseg != kNoSeg) {
+      const unsigned pend = __ballot_sync(0xffffffffu, lane < (int)k && w.pv > s_thr[w.pseg]);
+      if (pend) cta_insert(pend, w.pv, w.pseg, lane, k, s_thr, s_list, s_lock);
+    }
+    w.pv = w.v;
+    w.pseg = w.seg;
   }
   w.v = 0;
   w.thr = 0;
@@ -151,21 +212,30 @@ __device__ __forceinline__ void wl_offer(uint64_t key, uint32_t seg, WarpList& w
   const bool mine = seg == w.seg;
   unsigned pend = __ballot_sync(0xffffffffu, !mine || key > w.thr);   // key 0 carries w.seg
   if (pend == 0) return;
+  K2_COUNT(0);
   const unsigned other = pend & __ballot_sync(0xffffffffu, !mine);
   if (other) {
     const uint32_t s0 = __shfl_sync(0xffffffffu, seg, __ffs(other) - 1);
     const unsigned same0 = other & __ballot_sync(0xffffffffu, seg == s0);
     if (same0 == other && other == pend) {
       // the warp has moved on to segment s0: publish the old list, adopt s0
+      K2_COUNT(2);
       wl_flush(w, lane, k, s_thr, s_list, s_lock);
       w.seg = s0;
     } else {
       // mixed segments in one batch (segment boundary / unordered input)
+      K2_COUNT(3);
       const bool in_other = (other >> lane) & 1u;
       const unsigned o2 = __ballot_sync(0xffffffffu, in_other && key > s_thr[seg]);
       if (o2) cta_insert(o2, key, seg, lane, k, s_thr, s_list, s_lock);
       pend &= ~other;
     }
+  }
+  if (__popc(pend) >= kBatchMerge) {
+    K2_COUNT(1);
+    w.v = list_merge_batch(w.v, (pend >> lane) & 1u ? key : 0ull, lane, k);
+    w.thr = warp_list_min(w.v, (int)k);
+    return;
   }
   while (pend) {
     const int l = __ffs(pend) - 1;
@@ -186,12 +256,16 @@ struct K2Shared {
   int* lock;
 };
 
+// Stage slots (k keys + segment id each) after the CTA's shared tables:
+// current lists in slots [0, n_warps), previous lists in [n_warps, 2 n_warps).
+constexpr uint32_t kStageSlots = 48;
+
 __host__ __device__ inline size_t k2_tail_bytes(const ArchParams& a, uint32_t n_var,
                                                 uint32_t n_seg, uint32_t k, bool vt_smem) {
   size_t b = k2_arch_bytes(a);
   if (vt_smem) b += (size_t)n_var * a.n * sizeof(occx_vent_t);
   return b + (size_t)n_seg * 8 + (size_t)n_seg * k * 8 + (size_t)n_seg * 4 + 16 +
-         (size_t)32 * (OCCX_MAX_K + 1) * 8;
+         (size_t)kStageSlots * (OCCX_MAX_K + 1) * 8;
 }
 
 template <int MODE, bool VT_SMEM>
@@ -227,10 +301,13 @@ __device__ inline K2Shared k2_setup(const ScoreParams& p, unsigned char* base) {
 // the staged lists into the shared table alone (no lock traffic), then
 // the table is written out.  `stage` holds n_warps x (k keys + segment).
 __device__ inline void k2_stage(const WarpList& wl, int lane, uint32_t k, uint64_t* stage,
-                                uint32_t slot) {
+                                uint32_t slot, uint32_t n_warps) {
   uint64_t* row = stage + (size_t)slot * (OCCX_MAX_K + 1);
   if (lane < (int)k) row[lane] = wl.v;
   if (lane == 0) row[OCCX_MAX_K] = wl.seg;
+  row += (size_t)n_warps * (OCCX_MAX_K + 1);
+  if (lane < (int)k) row[lane] = wl.pv;
+  if (lane == 0) row[OCCX_MAX_K] = wl.pseg;
 }
 
 __device__ inline void k2_merge_staged(const uint64_t* stage, uint32_t n_slots, uint32_t k,
@@ -271,7 +348,7 @@ __device__ __forceinline__ void k2_process4(const K2Shared& s, K2Cache& cc, Warp
   } else {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      if (!__all_sync(0xffffffffu, k2_hit(cc, r[j]))) k2_fill<VT_SMEM>(s.c, r[j], cc);
+      if (!__all_sync(0xffffffffu, k2_hit(cc, r[j]))) { K2_COUNT(5); k2_fill<VT_SMEM>(s.c, r[j], cc); }
       key[j] = k2_key<MODE>(s.c, cc, r[j], inv - 32u * j);
       seg[j] = cc.seg;
     }
@@ -284,9 +361,15 @@ __device__ __forceinline__ void k2_process4(const K2Shared& s, K2Cache& cc, Warp
   for (int j = 0; j < 4; ++j)
     any = any | (((uint32_t)(key[j] >> 32) != 0u) & ((seg[j] != wl.seg) | (key[j] > thr)));
   if (__any_sync(0xffffffffu, any)) {
+#ifdef OCCX_K2_TIMING
+    const long long c0 = k2_clk();
+#endif
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       wl_offer(key[j], key[j] ? seg[j] : wl.seg, wl, lane, k, s.thr, s.list, s.lock);
+#ifdef OCCX_K2_TIMING
+    K2_ADD(6, k2_clk() - c0);
+#endif
   }
 }
 
@@ -304,7 +387,7 @@ __global__ void __launch_bounds__(kLdgThreads, 2) score_topk_ldg_kernel(const __
   const uint64_t end = begin + p.chunk < p.n ? begin + p.chunk : p.n;
   constexpr int kTile = kLdgThreads * kLdgUnroll;
   static_assert(kLdgUnroll == 4, "k2_process4");
-  WarpList wl{0, 0, kNoSeg};
+  WarpList wl{0, 0, kNoSeg, kNoSeg, 0};
   K2Cache cc;
   cc.x = cc.z = cc.w = 0xffffffffu;
   k2_fill<VT_SMEM>(s.c, make_uint4(0xffffffffu, 0, 0, 0xffffffffu), cc);
@@ -320,9 +403,9 @@ __global__ void __launch_bounds__(kLdgThreads, 2) score_topk_ldg_kernel(const __
   }
   uint64_t* stage = reinterpret_cast<uint64_t*>(const_cast<int*>(s.lock + p.n_seg)) + 1;
   stage = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(stage) + 7) & ~uintptr_t(7));
-  k2_stage(wl, lane, p.k, stage, threadIdx.x >> 5);
+  k2_stage(wl, lane, p.k, stage, threadIdx.x >> 5, kLdgThreads / 32);
   __syncthreads();
-  if (threadIdx.x < 32) k2_merge_staged(stage, kLdgThreads / 32, p.k, s.thr, s.list, s.lock);
+  if (threadIdx.x < 32) k2_merge_staged(stage, 2 * kLdgThreads / 32, p.k, s.thr, s.list, s.lock);
   __syncthreads();
   k2_flush(p, s);
 }
@@ -456,6 +539,7 @@ __device__ __forceinline__ uint4 ig_record(const IgCache& c, const uint32_t* poo
 
 constexpr int kIgThreads = 768;                 // 24 warps per SM: 0.83 ms vs 0.94 (16) and 0.92 (32) on config 5
 constexpr int kIgWarps = kIgThreads / 32;
+static_assert(2 * kIgWarps <= (int)kStageSlots, "stage slots");
 constexpr int kIgTab = 1024;                    // per-warp separable-table words (|REGS| + |SMEM|)
 
 // ---- separable block tables (implicit grid) --------------------------------
@@ -565,7 +649,7 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
   const K2Shared s = k2_setup<MODE, VT_SMEM>(p, smem);
   uint64_t* stage = reinterpret_cast<uint64_t*>(const_cast<int*>(s.lock + p.n_seg)) + 1;
   stage = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(stage) + 7) & ~uintptr_t(7));
-  uint32_t* sep_tab = reinterpret_cast<uint32_t*>(stage + 32 * (OCCX_MAX_K + 1));
+  uint32_t* sep_tab = reinterpret_cast<uint32_t*>(stage + kStageSlots * (OCCX_MAX_K + 1));
   const uint32_t* pool = q.pool;
   if (q.pool_smem) {
     uint32_t* sp = sep_tab + kIgWarps * q.sep_words;
@@ -579,7 +663,7 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
   const uint64_t begin = q.begin + (uint64_t)blockIdx.x * p.chunk;
   const uint64_t stop = q.begin + p.n;
   const uint64_t end = begin + p.chunk < stop ? begin + p.chunk : stop;
-  WarpList wl{0, 0, kNoSeg};
+  WarpList wl{0, 0, kNoSeg, kNoSeg, 0};
   K2Cache cc;
   cc.x = cc.z = cc.w = 0xffffffffu;
   k2_fill<VT_SMEM>(s.c, make_uint4(0xffffffffu, 0, 0, 0xffffffffu), cc);
@@ -753,9 +837,9 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
     }
     k2_process4<MODE, VT_SMEM>(s, cc, wl, r, kIdxMask - q.key_off - g0, lane, p.k);
   }
-  k2_stage(wl, lane, p.k, stage, threadIdx.x >> 5);
+  k2_stage(wl, lane, p.k, stage, threadIdx.x >> 5, kIgWarps);
   __syncthreads();
-  if (threadIdx.x < 32) k2_merge_staged(stage, kIgWarps, p.k, s.thr, s.list, s.lock);
+  if (threadIdx.x < 32) k2_merge_staged(stage, 2 * kIgWarps, p.k, s.thr, s.list, s.lock);
   __syncthreads();
   k2_flush(p, s);
 }
@@ -808,6 +892,27 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       : "memory");
 }
 
+#ifdef OCCX_K2_TIMING
+// experiment-only (scratch/k2_timing.sh): per-CTA {start, end, smid, tiles}
+__device__ uint64_t g_k2_timing[4 * 1024];
+}  // namespace
+extern "C" int occx_debug_k2_timing(uint64_t* out, int n) {
+  return cudaMemcpyFromSymbol(out, g_k2_timing, (size_t)n * 4 * 8) == cudaSuccess ? 0 : 6;
+}
+extern "C" int occx_debug_k2_counts(uint64_t* out, int n, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_k2_cnt, (size_t)n * 8 * 8) != cudaSuccess) return 6;
+  if (reset) {
+    static unsigned long long zero[16 * 1024];
+    if (cudaMemcpyToSymbol(g_k2_cnt, zero, 8 * 1024 * 8) != cudaSuccess) return 6;
+    if (cudaMemcpyToSymbol(g_k2_hist, zero, sizeof(zero)) != cudaSuccess) return 6;
+  }
+  return 0;
+}
+extern "C" int occx_debug_k2_hist(uint64_t* out, int n) {
+  return cudaMemcpyFromSymbol(out, g_k2_hist, (size_t)n * 16 * 8) == cudaSuccess ? 0 : 6;
+}
+namespace {
+#endif
 template <int MODE, bool VT_SMEM, int SL>
 __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __grid_constant__ ScoreParams p) {
   constexpr int kTmaSlices = SL;
@@ -833,6 +938,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
   const uint64_t begin = (uint64_t)blockIdx.x * p.chunk;
   const uint64_t end = begin + p.chunk < p.n ? begin + p.chunk : p.n;
   const uint32_t n_tiles = begin < end ? (uint32_t)((end - begin + kTmaTile - 1) / kTmaTile) : 0u;
+#ifdef OCCX_K2_TIMING
+  if (threadIdx.x == 0) {
+    uint64_t t0; uint32_t sm;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    g_k2_timing[blockIdx.x * 4 + 0] = t0;
+    g_k2_timing[blockIdx.x * 4 + 2] = sm;
+    g_k2_timing[blockIdx.x * 4 + 3] = n_tiles;
+  }
+#endif
   if (warp == 0) {
     if (lane == 0) {
       uint64_t policy;
@@ -847,7 +962,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
       }
     }
   } else {
-    WarpList wl{0, 0, kNoSeg};
+    WarpList wl{0, 0, kNoSeg, kNoSeg, 0};
     K2Cache cc;
     cc.x = cc.z = cc.w = 0xffffffffu;
     k2_fill<VT_SMEM>(s.c, make_uint4(0xffffffffu, 0, 0, 0xffffffffu), cc);
@@ -855,7 +970,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
       const uint32_t st = t % kTmaStages;
       const uint64_t tb = begin + (uint64_t)t * kTmaTile;
       const uint32_t cnt = (uint32_t)min((uint64_t)kTmaTile, end - tb);
+#ifdef OCCX_K2_TIMING
+      const long long w0 = k2_clk();
+#endif
       mbar_wait(&full[st], (t / kTmaStages) & 1u);
+#ifdef OCCX_K2_TIMING
+      K2_ADD(7, k2_clk() - w0);
+#endif
       const uint4* tile = ring + (size_t)st * kTmaTile;
       // warp w takes kTmaSlices contiguous 128-record slices of the tile, so
       // its (T, variant, arch) cache sees kTmaSlices x 128 consecutive records
@@ -877,17 +998,32 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);      // records are in registers
+#ifdef OCCX_K2_TIMING
+      const long long p0 = k2_clk();
+#endif
 #pragma unroll
       for (int h = 0; h < kTmaSlices; ++h)
         k2_process4<MODE, VT_SMEM>(s, cc, wl, r[h], kIdxMask - p.index_base - tb - slice - 128u * h,
                                    lane, p.k);
+#ifdef OCCX_K2_TIMING
+      if (lane == 0)
+        atomicAdd(&g_k2_hist[blockIdx.x * 16 + (t * 16u) / n_tiles], (unsigned long long)(k2_clk() - p0));
+#endif
     }
-    k2_stage(wl, lane, p.k, stage, warp - 1);
+    k2_stage(wl, lane, p.k, stage, warp - 1, kTmaConsumerWarps);
   }
   __syncthreads();
-  if (warp == 1) k2_merge_staged(stage, kTmaConsumerWarps, p.k, s.thr, s.list, s.lock);
+  if (warp == 1) k2_merge_staged(stage, 2 * kTmaConsumerWarps, p.k, s.thr, s.list, s.lock);
   __syncthreads();
   k2_flush(p, s);
+#ifdef OCCX_K2_TIMING
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    g_k2_timing[blockIdx.x * 4 + 1] = t1;
+  }
+#endif
 }
 
 // ---------------------------------------------------------------------------
