@@ -386,9 +386,29 @@ def secondary_space_api(cfg, mode: str, steps: int = 10):
     e1.record(stream)
     torch.cuda.synchronize()
     k_ms = e0.elapsed_time(e1) / steps
-    return {"kernel": "score_space_kernel (K2i, implicit grid, no K3)", "kernel_ms": k_ms,
-            "value": plan.total / (k_ms / 1e3), "unit": UNIT, "bound": "integer issue",
-            "note": "no candidate records in HBM; see profiles/r01_k2i_ncu_full.json"}
+    out = {"kernel": "score_space_kernel (K2i, implicit grid, no K3)", "kernel_ms": k_ms,
+           "value": plan.total / (k_ms / 1e3), "unit": UNIT, "bound": "integer issue",
+           "note": "no candidate records in HBM; see profiles/r01_k2i_ncu_full.json"}
+    # issue roofline: the ncu capture's warp-instruction count per launch (same
+    # workload) over the live kernel time, against 4 issue slots/SM/clock
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_k2i_ncu_full.json")) as fh:
+            prof = json.load(fh)
+        if prof.get("workload") == cfg.name:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+            mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+            achieved = prof["warp_instructions"] / (k_ms / 1e3) / 1e9
+            peak = 4 * sms * mhz / 1e3
+            out["roofline"] = {"bound": "issue", "achieved": achieved, "peak": peak,
+                               "unit": "G warp-instructions/s", "frac": achieved / peak,
+                               "instructions_per_launch": prof["warp_instructions"],
+                               "peak_source": f"4 issue slots x {sms} SMs x {mhz} MHz (max SM clock)"}
+    except Exception as exc:
+        out["roofline"] = {"error": repr(exc)[:160]}
+    return out
 
 
 # ---------------------------------------------------------------------------
