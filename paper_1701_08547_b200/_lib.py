@@ -137,6 +137,8 @@ def ctx(device: int | None = None) -> int:
         check(load().occx_ctx_create(dev, ctypes.byref(out)), "occx_ctx_create")
         with _lock:
             h = _ctx.setdefault(dev, out.value)
+        if h != out.value:          # another thread won the race: drop ours
+            load().occx_ctx_destroy(out)
     return h
 
 
