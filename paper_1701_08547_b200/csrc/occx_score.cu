@@ -858,7 +858,6 @@ template <int SL> struct TmaRing {
   static constexpr size_t kBytes = (size_t)kStages * kTile * 16;
 };
 constexpr int kTmaTile = TmaRing<1>::kTile;     // chunk granularity (multiple of both tiles)
-constexpr uint64_t kTmaBigCall = 1ull << 28;    // candidates per call above which SL = 2
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -1380,8 +1379,12 @@ extern "C" int occx_score_topk(const occx_ctx* ctx, const occx_arch_t* h_archs, 
   const int feed = score_feed();
   p.vt_smem = ((uint64_t)n_var * n_arch <= (uint64_t)kVtSmemMax) ? 1u : 0u;
   size_t smem = k2_tail_bytes(p.archs, n_var, n_seg, k, p.vt_smem != 0);
-  // two slices per warp for big calls when the deeper ring fits
-  int sl = (feed == kFeedTma && n >= kTmaBigCall &&
+  // two slices per warp (64 KB stages, 192 KB in flight per SM) whenever the
+  // ring fits: per-SM bandwidth is bytes-in-flight bound (config 2: 0.123 ->
+  // 0.107 ms, config 4: 0.309 -> 0.298 ms vs one slice).  OCCX_K2_SL=1 forces one.
+  const char* sl_env = std::getenv("OCCX_K2_SL");
+  const bool one_slice = sl_env && sl_env[0] == '1';
+  int sl = (feed == kFeedTma && !one_slice &&
             smem + TmaRing<2>::kBytes + 2 * TmaRing<2>::kStages * 8 <= (size_t)ctx->max_smem_optin)
                ? 2 : 1;
   if (feed == kFeedTma)
