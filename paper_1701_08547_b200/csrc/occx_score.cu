@@ -118,8 +118,9 @@ __device__ __forceinline__ uint64_t warp_sort_desc(uint64_t x, int lane) {
 // one at a time (keys are unique).  Lanes >= k come back 0.
 constexpr int kBatchMerge = 6;
 
-__device__ __noinline__ uint64_t list_merge_batch(uint64_t list, uint64_t x, int lane, uint32_t k) {
-  x = warp_sort_desc(x, lane);
+// Merge two descending top-k lists held in lanes 0..k-1 (lanes >= k of x may
+// hold anything): the top k of both, descending, lanes >= k zero.
+__device__ __noinline__ uint64_t list_merge_sorted(uint64_t list, uint64_t x, int lane, uint32_t k) {
   const uint64_t xr = __shfl_sync(0xffffffffu, x, ((int)k - 1 - lane) & 31);
   uint64_t y = lane < (int)k ? (list > xr ? list : xr) : 0ull;
   if ((k & (k - 1)) == 0) {
@@ -131,6 +132,10 @@ __device__ __noinline__ uint64_t list_merge_batch(uint64_t list, uint64_t x, int
     y = warp_sort_desc(y, lane);
   }
   return y;
+}
+
+__device__ __forceinline__ uint64_t list_merge_batch(uint64_t list, uint64_t x, int lane, uint32_t k) {
+  return list_merge_sorted(list, warp_sort_desc(x, lane), lane, k);
 }
 
 __device__ __forceinline__ void cta_insert(unsigned pend, uint64_t key, uint32_t seg,
@@ -1028,7 +1033,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
 // ---------------------------------------------------------------------------
 // K3: merge n_lists tables [n_lists][n_seg][k] -> [n_seg][k]; one CTA/segment
 // ---------------------------------------------------------------------------
-constexpr int kMergeThreads = 256;
+constexpr int kMergeThreads = 1024;
 
 __global__ void __launch_bounds__(kMergeThreads)
 topk_merge_kernel(const uint64_t* __restrict__ lists, uint32_t n_lists, uint32_t n_seg, uint32_t k,
@@ -1039,14 +1044,21 @@ topk_merge_kernel(const uint64_t* __restrict__ lists, uint32_t n_lists, uint32_t
   constexpr int kWarps = kMergeThreads / 32;
   uint64_t mine = 0;
   const uint64_t total = (uint64_t)n_lists * k;
-  for (uint64_t b = (uint64_t)warp * 32; b < total; b += (uint64_t)kWarps * 32) {
-    const uint64_t i = b + lane;
-    uint64_t key = 0;
-    if (i < total) {
-      const uint64_t l = i / k, j = i - l * k;
-      key = lists[(l * n_seg + seg) * k + j];
-    }
+  const uint64_t step = (uint64_t)kWarps * 32;
+  auto load = [&](uint64_t i) -> uint64_t {
+    if (i >= total) return 0ull;
+    const uint64_t l = i / k, j = i - l * k;
+    return lists[(l * n_seg + seg) * k + j];
+  };
+  uint64_t next = load((uint64_t)warp * 32 + lane);         // one batch ahead
+  for (uint64_t b = (uint64_t)warp * 32; b < total; b += step) {
+    const uint64_t key = next;
+    next = load(b + step + lane);
     unsigned pend = __ballot_sync(0xffffffffu, key > warp_list_min(mine, (int)k));
+    if (__popc(pend) >= kBatchMerge) {
+      mine = list_merge_batch(mine, (pend >> lane) & 1u ? key : 0ull, lane, k);
+      pend = 0;
+    }
     while (pend) {
       const int src = __ffs(pend) - 1;
       pend &= pend - 1;
@@ -1056,20 +1068,17 @@ topk_merge_kernel(const uint64_t* __restrict__ lists, uint32_t n_lists, uint32_t
   }
   if (lane < (int)k) s_w[warp][lane] = mine;
   __syncthreads();
-  if (warp == 0) {
-    uint64_t acc = (lane < (int)k) ? s_w[0][lane] : 0ull;
-    for (int w = 1; w < kWarps; ++w) {
-      const uint64_t key = (lane < (int)k) ? s_w[w][lane] : 0ull;
-      unsigned pend = __ballot_sync(0xffffffffu, key > warp_list_min(acc, (int)k));
-      while (pend) {
-        const int src = __ffs(pend) - 1;
-        pend &= pend - 1;
-        const uint64_t kk = __shfl_sync(0xffffffffu, key, src);
-        if (kk > warp_list_min(acc, (int)k)) warp_list_insert(acc, kk, (int)k, lane);
-      }
+  // the warps' lists are sorted: a tree of pairwise sorted merges
+  for (int stride = 1; stride < kWarps; stride <<= 1) {
+    if (warp % (2 * stride) == 0) {
+      const uint64_t a = (lane < (int)k) ? s_w[warp][lane] : 0ull;
+      const uint64_t b = (lane < (int)k) ? s_w[warp + stride][lane] : 0ull;
+      const uint64_t m = list_merge_sorted(a, b, lane, k);
+      if (lane < (int)k) s_w[warp][lane] = m;
     }
-    if (lane < (int)k) out[(size_t)seg * k + lane] = acc;
+    __syncthreads();
   }
+  if (warp == 0 && lane < (int)k) out[(size_t)seg * k + lane] = s_w[0][lane];
 }
 
 // ---------------------------------------------------------------------------
