@@ -324,8 +324,14 @@ __device__ inline void k2_merge_staged(const uint64_t* stage, uint32_t n_slots, 
     const uint32_t seg = (uint32_t)row[OCCX_MAX_K];
     if (seg == kNoSeg) continue;
     const uint64_t key = lane < (int)k ? row[lane] : 0ull;
-    const unsigned pend = __ballot_sync(0xffffffffu, key > s_thr[seg]);
-    if (pend) cta_insert(pend, key, seg, lane, k, s_thr, s_list, s_lock);
+    if (!__any_sync(0xffffffffu, key > s_thr[seg])) continue;
+    // one warp merges after the CTA barrier: no lock; staged lists are sorted
+    uint64_t mine = lane < (int)k ? s_list[seg * k + lane] : 0ull;
+    mine = list_merge_sorted(mine, key, lane, k);
+    if (lane < (int)k) s_list[seg * k + lane] = mine;
+    const uint64_t thr = warp_list_min(mine, (int)k);
+    if (lane == 0) s_thr[seg] = thr;
+    __syncwarp();
   }
 }
 
