@@ -933,21 +933,31 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
   uint4* ring = reinterpret_cast<uint4*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTmaRingBytes);
   uint64_t* empty = full + kTmaStages;
-  const K2Shared s = k2_setup<MODE, VT_SMEM>(p, smem + kTmaRingBytes + 2 * kTmaStages * 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint64_t* stage = reinterpret_cast<uint64_t*>(const_cast<int*>(s.lock + p.n_seg)) + 1;
-  stage = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(stage) + 7) & ~uintptr_t(7));
+  const uint64_t begin = (uint64_t)blockIdx.x * p.chunk;
+  const uint64_t end = begin + p.chunk < p.n ? begin + p.chunk : p.n;
+  const uint32_t n_tiles = begin < end ? (uint32_t)((end - begin + kTmaTile - 1) / kTmaTile) : 0u;
+  const uint32_t first = n_tiles < (uint32_t)kTmaStages ? n_tiles : (uint32_t)kTmaStages;
+  uint64_t policy = 0;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kTmaStages; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], kTmaConsumerWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    // the first ring round needs no free slot: start it before the table setup
+    for (uint32_t t = 0; t < first; ++t) {
+      const uint64_t tb = begin + (uint64_t)t * kTmaTile;
+      const uint32_t cnt = (uint32_t)min((uint64_t)kTmaTile, end - tb);
+      mbar_expect_tx(&full[t], cnt * 16u);
+      tma_load_1d(ring + (size_t)t * kTmaTile, p.cand + tb, cnt * 16u, &full[t], policy);
+    }
   }
+  const K2Shared s = k2_setup<MODE, VT_SMEM>(p, smem + kTmaRingBytes + 2 * kTmaStages * 8);
+  uint64_t* stage = reinterpret_cast<uint64_t*>(const_cast<int*>(s.lock + p.n_seg)) + 1;
+  stage = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(stage) + 7) & ~uintptr_t(7));
   __syncthreads();
-  const uint64_t begin = (uint64_t)blockIdx.x * p.chunk;
-  const uint64_t end = begin + p.chunk < p.n ? begin + p.chunk : p.n;
-  const uint32_t n_tiles = begin < end ? (uint32_t)((end - begin + kTmaTile - 1) / kTmaTile) : 0u;
 #ifdef OCCX_K2_TIMING
   if (threadIdx.x == 0) {
     uint64_t t0; uint32_t sm;
@@ -960,9 +970,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
 #endif
   if (warp == 0) {
     if (lane == 0) {
-      uint64_t policy;
-      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-      for (uint32_t t = 0; t < n_tiles; ++t) {
+      for (uint32_t t = first; t < n_tiles; ++t) {
         const uint32_t st = t % kTmaStages;
         mbar_wait(&empty[st], ((t / kTmaStages) & 1u) ^ 1u);
         const uint64_t tb = begin + (uint64_t)t * kTmaTile;
