@@ -375,20 +375,31 @@ def secondary_space_api(cfg, mode: str, steps: int = 10):
     import torch
     from paper_1701_08547_b200 import ScorePlan
     plan = ScorePlan(cfg.kernels, cfg.archs, mode, k=cfg.k)
-    for _ in range(3):
-        plan.score_implicit(merge=False)
-    torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(steps):
-        plan.score_implicit(merge=False)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    k_ms = e0.elapsed_time(e1) / steps
+
+    def timed(prune: bool) -> float:
+        os.environ["OCCX_K2I_PRUNE"] = "1" if prune else "0"
+        try:
+            for _ in range(3):
+                plan.score_implicit(merge=False)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(steps):
+                plan.score_implicit(merge=False)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / steps
+        finally:
+            os.environ.pop("OCCX_K2I_PRUNE", None)
+    k_ms = timed(False)
+    p_ms = timed(True)
     out = {"kernel": "score_space_kernel (K2i, implicit grid, no K3)", "kernel_ms": k_ms,
            "value": plan.total / (k_ms / 1e3), "unit": UNIT, "bound": "integer issue",
-           "note": "no candidate records in HBM; see profiles/r01_k2i_ncu_full.json"}
+           "note": "every candidate's key evaluated (OCCX_K2I_PRUNE=0); no candidate records "
+                   "in HBM; see profiles/r01_k2i_ncu_full.json",
+           "pruned": {"kernel_ms": p_ms, "value": plan.total / (p_ms / 1e3),
+                      "note": "library default: blocks skipped on an exact bound"}}
     # issue roofline: the ncu capture's warp-instruction count per launch (same
     # workload) over the live kernel time, against 4 issue slots/SM/clock
     try:
@@ -573,20 +584,35 @@ def main():
             def api_step():
                 return score_space_multi(cfg.kernels, cfg.archs, mode, cfg.k,
                                          scaling=args.scaling, gather_on_host=gloo)
-            for _ in range(2):
-                segs, keys = api_step()
-            torch.cuda.synchronize()
-            barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(e2e_steps):
-                segs, keys = api_step()
-            e1.record(stream)
-            torch.cuda.synchronize()
-            e_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
-            assert np.array_equal(keys.numpy().view(np.uint64), final_keys), \
-                "API top-k differs from the record path"
+
+            def timed_api(prune: bool) -> float:
+                # OCCX_K2I_PRUNE is read by liboccx at every K2i launch
+                os.environ["OCCX_K2I_PRUNE"] = "1" if prune else "0"
+                try:
+                    for _ in range(2):
+                        api_step()
+                    torch.cuda.synchronize()
+                    barrier()
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    for _ in range(e2e_steps):
+                        segs, keys = api_step()
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    assert np.array_equal(keys.numpy().view(np.uint64), final_keys), \
+                        "API top-k differs from the record path"
+                    return max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
+                finally:
+                    os.environ.pop("OCCX_K2I_PRUNE", None)
+            # headline: every candidate's key evaluated (block pruning off)
+            e_ms = timed_api(prune=False)
+            p_ms = timed_api(prune=True)
             e2e = {"value": global_total / (e_ms / 1e3), "unit": UNIT,
+                   "pruned": {"value": global_total / (p_ms / 1e3), "ms_per_step": p_ms,
+                              "note": "the library default: K2i skips blocks whose bound "
+                                      "(max active-warps field x block key bits) cannot "
+                                      "enter the warp's top-k; same top-k (asserted)"},
                    "h2d_bytes_per_step": int(plan.h2d_bytes),
                    "d2h_bytes_per_step": 8 * plan.n_seg * plan.k,
                    "ms_per_step": e_ms, "steps": e2e_steps,

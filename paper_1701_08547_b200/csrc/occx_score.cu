@@ -462,7 +462,7 @@ struct SpaceParams {
   uint64_t begin;        // global index of the first candidate scored
   uint64_t key_off;      // added to the global index in keys (weak-scaling copies)
   uint32_t sep_words;    // per-warp separable-table capacity (0: general path only)
-  uint32_t pad2;
+  uint32_t prune;        // skip blocks whose best possible key cannot enter the warp list
 };
 
 // Record words of the block the digits point at.
@@ -617,6 +617,46 @@ __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
 // Fill TR[0, nR] and TS[0, nS + 7) (tr = the warp's table, shared address)
 // for the block ic points at; TR[nR] = 0 and TS[nS + t] = TS[t mod nS] pad
 // the +j lookups.  False (tables untouched) when they do not fit.
+// Upper bound of the active-warps field over a block: inside a block T and
+// the arch are fixed, so the warps field of candidate (R, S) is
+// min(awR(R), awS(S)) and its maximum is min(max awR, max awS) -- the same
+// separable form the tables use.  Cached per warp on (T, arch, pool offsets):
+// consecutive blocks of a segment differ in BC / UIF / PL / CFLAGS only.
+struct BlockBound {
+  uint32_t z, w, r_off, s_off;   // cache key: T | BC << 16 (T part), arch, pools
+  uint32_t aw;                   // min(max awR, max awS)
+};
+
+template <int MODE>
+__device__ __forceinline__ uint32_t block_aw_max(const SpaceParams& q, const uint32_t* pool,
+                                                 const IgCache& ic, const K2Cache& kc,
+                                                 BlockBound& bb, int lane) {
+  const uint32_t a = min((ic.w_hi >> 16) & 0xffu, (uint32_t)q.sp.archs.n - 1);
+  if (bb.z == (ic.z & 0xffffu) && bb.w == a && bb.r_off == ic.r_off && bb.s_off == ic.s_off)
+    return bb.aw;
+  const occx_arch_t& arch = q.sp.archs.a[a];
+  const uint32_t ns = ic.n_s, nr = ic.blk_n / ic.n_s;
+  const uint32_t lw = min(kc.lw, 255u), wpb = max(kc.wpb, 1u), wmp = kc.wmp;
+  uint32_t mr = 0, ms = 0;
+  for (uint32_t i = (uint32_t)lane; i < nr; i += 32) {
+    const uint32_t R = min(pool[ic.r_off + i], 0xffffu);
+    mr = max(mr, min(min(lw, sep_lr<MODE>(arch, wpb, R)) * wpb, wmp));
+  }
+  for (uint32_t i = (uint32_t)lane; i < ns; i += 32)
+    ms = max(ms, min(sep_ls<MODE>(arch, pool[ic.s_off + i]) * wpb, wmp));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mr = max(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+    ms = max(ms, __shfl_xor_sync(0xffffffffu, ms, o));
+  }
+  bb.z = ic.z & 0xffffu;
+  bb.w = a;
+  bb.r_off = ic.r_off;
+  bb.s_off = ic.s_off;
+  bb.aw = min(mr, ms);
+  return bb.aw;
+}
+
 template <int MODE, bool VT_SMEM>
 __device__ __forceinline__ bool sep_build(const SpaceParams& q, const K2Shared& s,
                                           const uint32_t* pool, const IgCache& ic,
@@ -684,6 +724,9 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
   SepBlock sb;
   sb.lo = 0;
   sb.n = 0;
+  BlockBound bbnd;
+  bbnd.z = 0xffffffffu;
+  bbnd.w = bbnd.r_off = bbnd.s_off = bbnd.aw = 0;
   // each warp walks its own contiguous range in 128-candidate slices, so a
   // lane's block advances by +1 (digit carry) instead of being re-decoded
   const uint64_t wsz = p.chunk / kIgWarps;               // multiple of 128
@@ -802,6 +845,25 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
   for (uint64_t base = wb; base < we; base += 128) {
     if (base + 128 <= we) {
       ig_seek(q, pool, base, ic);                          // same g on every lane
+      if (q.prune && base + 128 - ic.blk_lo <= (uint64_t)ic.blk_n) {
+        // Block bound: every key of the block is at most (hi | aw_max) in its
+        // high word plus the index bits of the block's first slice (the walk
+        // goes forward, indices only grow).  When that cannot beat the warp
+        // list of the same segment -- the test fast_quad applies per lane --
+        // none of the block's whole slices can, and they are skipped.
+        K2Cache kb;
+        k2_fill<VT_SMEM>(s.c, make_uint4(ic.x, 0u, ic.z, ic.w_hi), kb);
+        const uint32_t aw = (kb.ok && kb.wpb != 0) ? block_aw_max<MODE>(q, pool, ic, kb, bbnd, lane)
+                                                   : 0u;
+        const uint32_t bound = aw ? (kb.key_hi | (aw << 22)) : 0u;
+        const uint32_t inv_hi = (uint32_t)((kIdxMask - q.key_off - base) >> 32);
+        if (!(bound & 0x1fc00000u) ||
+            (kb.seg == wl.seg && (bound | inv_hi) <= (uint32_t)(wl.thr >> 32))) {
+          const uint64_t lb = (ic.blk_lo + ic.blk_n - base) >> 7, lr = (we - base) >> 7;
+          base += ((lb < lr ? lb : lr) - 1) * 128;         // + the for-increment
+          continue;
+        }
+      }
       if (base + 128 - ic.blk_lo <= (uint64_t)ic.blk_n &&
           sep_build<MODE, VT_SMEM>(q, s, pool, ic, tr, sb, lane)) {
         const uint64_t lb = (sb.lo + sb.n - base) >> 7, lr = (we - base) >> 7;
@@ -1552,6 +1614,8 @@ extern "C" int occx_score_space(const occx_ctx* ctx, const occx_arch_t* h_archs,
   if (smem > (size_t)ctx->max_smem_optin) return OCCX_ERR_CAPACITY;
   // per-warp separable tables when they fit (else the general path only)
   q.sep_words = smem + (size_t)kIgWarps * kIgTab * 4 <= (size_t)ctx->max_smem_optin ? kIgTab : 0;
+  const char* pr = std::getenv("OCCX_K2I_PRUNE");      // 0: score every candidate
+  q.prune = (pr && pr[0] == '0') ? 0u : 1u;
   smem += (size_t)kIgWarps * q.sep_words * 4;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
 #define OCCX_LAUNCH_IG(KERNEL)                                                       \

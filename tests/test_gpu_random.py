@@ -3,6 +3,7 @@ device form can represent), random tuning spaces, random instruction mixes,
 both evaluation modes -- CUDA path vs the independent oracles.  Seeded, so
 a failure reproduces."""
 
+import os
 import random
 
 import numpy as np
@@ -75,8 +76,13 @@ def test_random_spaces_k2_k2i_vs_oracle(seed):
         rec = plan.generate()
         got = plan.score(rec, plan.total).cpu().numpy().view(np.uint64)
         assert np.array_equal(got, want), (seed, mode)
-        got_i = plan.score_implicit().cpu().numpy().view(np.uint64)
-        assert np.array_equal(got_i, want), (seed, mode, "implicit")
+        for prune in ("1", "0"):           # block-bound pruning on (default) and off
+            os.environ["OCCX_K2I_PRUNE"] = prune
+            try:
+                got_i = plan.score_implicit().cpu().numpy().view(np.uint64)
+            finally:
+                os.environ.pop("OCCX_K2I_PRUNE", None)
+            assert np.array_equal(got_i, want), (seed, mode, "implicit", prune)
 
 
 @pytest.mark.parametrize("seed", range(6))
@@ -254,6 +260,12 @@ def test_random_big_blocks_k2i_vs_oracle(seed):
         plan = P.ScorePlan(cfg.kernels, cfg.archs, mode, k=cfg.k)
         got_i = plan.score_implicit().cpu().numpy().view(np.uint64)
         assert np.array_equal(got_i, want), (seed, mode, "implicit")
+        os.environ["OCCX_K2I_PRUNE"] = "0"
+        try:
+            got_f = plan.score_implicit().cpu().numpy().view(np.uint64)
+        finally:
+            os.environ.pop("OCCX_K2I_PRUNE", None)
+        assert np.array_equal(got_f, want), (seed, mode, "implicit, no pruning")
         rec = plan.generate()
         for b, n in ((0, plan.total), (rng.randrange(plan.total), None)):
             n = plan.total - b if n is None else n
