@@ -42,3 +42,25 @@ def test_two_rank_bench_line_gloo_harness(scaling):
     assert d["config"]["candidates"] == (2 * per if scaling == "weak" else 104_857_600)
     assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] == 3 * 3
     assert d["roofline"]["bound"] == "hbm" and d["clocks"]["sm_max_mhz"]
+
+
+def test_committed_bench_line_contract():
+    """The last GPU bench line committed under profiles/ carries every key of
+    the driver contract plus roofline / cpu_baseline / e2e (with the pruned
+    library default beside the every-key headline) and in-window clocks."""
+    with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                           "profiles", "r01_bench.json")) as fh:
+        d = json.loads(fh.read().strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+                "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert key in d, key
+    assert d["warmup"] >= 3 and d["gpu_launches"] > 0
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["cores"] >= 1
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert e["pruned"]["value"] >= e["value"] * 0.9
+    assert not set(d["clocks"]["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown",
+                                               "sw_thermal_slowdown"}
