@@ -138,6 +138,15 @@ __device__ __forceinline__ uint64_t list_merge_batch(uint64_t list, uint64_t x, 
   return list_merge_sorted(list, warp_sort_desc(x, lane), lane, k);
 }
 
+// s_thr[seg] is a lower bound of the segment's final k-th best key: the
+// CTA table's k-th best, or any warp's k-th best once its list is full (k
+// real keys of the segment).  Only ever raised; keys below it cannot enter
+// the result, so filters may drop them.
+__device__ __forceinline__ void thr_raise(volatile uint64_t* s_thr, uint32_t seg, uint64_t v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(const_cast<uint64_t*>(s_thr + seg)),
+            (unsigned long long)v);
+}
+
 __device__ __forceinline__ void cta_insert(unsigned pend, uint64_t key, uint32_t seg,
                                            int lane, uint32_t k, volatile uint64_t* s_thr,
                                            volatile uint64_t* s_list, int* s_lock) {
@@ -167,7 +176,7 @@ __device__ __forceinline__ void cta_insert(unsigned pend, uint64_t key, uint32_t
     const uint64_t thr = warp_list_min(mine, (int)k);
     __syncwarp();
     if (lane == 0) {
-      s_thr[sseg] = thr;
+      thr_raise(s_thr, sseg, thr);
       __threadfence_block();
       atomicExch(&s_lock[sseg], 0);
     }
@@ -200,7 +209,9 @@ __device__ __forceinline__ void wl_flush(WarpList& w, int lane, uint32_t k, vola
                                          volatile uint64_t* s_list, int* s_lock) {
   if (w.seg != kNoSeg) {
     if (w.pseg != kNoSeg) {
-      const unsigned pend = __ballot_sync(0xffffffffu, lane < (int)k && w.pv > s_thr[w.pseg]);
+      // ">=": s_thr may be this very list's k-th key (a shared bound), which must survive
+      const unsigned pend = __ballot_sync(0xffffffffu, lane < (int)k && w.pv != 0 &&
+                                                           w.pv >= s_thr[w.pseg]);
       if (pend) cta_insert(pend, w.pv, w.pseg, lane, k, s_thr, s_list, s_lock);
     }
     w.pv = w.v;
@@ -231,7 +242,7 @@ __device__ __forceinline__ void wl_offer(uint64_t key, uint32_t seg, WarpList& w
       // mixed segments in one batch (segment boundary / unordered input)
       K2_COUNT(3);
       const bool in_other = (other >> lane) & 1u;
-      const unsigned o2 = __ballot_sync(0xffffffffu, in_other && key > s_thr[seg]);
+      const unsigned o2 = __ballot_sync(0xffffffffu, in_other && key >= s_thr[seg]);
       if (o2) cta_insert(o2, key, seg, lane, k, s_thr, s_list, s_lock);
       pend &= ~other;
     }
@@ -240,8 +251,10 @@ __device__ __forceinline__ void wl_offer(uint64_t key, uint32_t seg, WarpList& w
     K2_COUNT(1);
     w.v = list_merge_batch(w.v, (pend >> lane) & 1u ? key : 0ull, lane, k);
     w.thr = warp_list_min(w.v, (int)k);
+    if (lane == 0 && w.thr > s_thr[w.seg]) thr_raise(s_thr, w.seg, w.thr);   // share the bound
     return;
   }
+  const uint64_t before = w.thr;
   while (pend) {
     const int l = __ffs(pend) - 1;
     pend &= pend - 1;
@@ -251,6 +264,7 @@ __device__ __forceinline__ void wl_offer(uint64_t key, uint32_t seg, WarpList& w
       w.thr = warp_list_min(w.v, (int)k);
     }
   }
+  if (lane == 0 && w.thr != before && w.thr > s_thr[w.seg]) thr_raise(s_thr, w.seg, w.thr);
 }
 
 // Shared-memory carve-up common to both feeds (after an optional TMA ring).
@@ -324,7 +338,7 @@ __device__ inline void k2_merge_staged(const uint64_t* stage, uint32_t n_slots, 
     const uint32_t seg = (uint32_t)row[OCCX_MAX_K];
     if (seg == kNoSeg) continue;
     const uint64_t key = lane < (int)k ? row[lane] : 0ull;
-    if (!__any_sync(0xffffffffu, key > s_thr[seg])) continue;
+    if (!__any_sync(0xffffffffu, key != 0 && key >= s_thr[seg])) continue;
     // one warp merges after the CTA barrier: no lock; staged lists are sorted
     uint64_t mine = lane < (int)k ? s_list[seg * k + lane] : 0ull;
     mine = list_merge_sorted(mine, key, lane, k);
@@ -857,8 +871,11 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
                                                    : 0u;
         const uint32_t bound = aw ? (kb.key_hi | (aw << 22)) : 0u;
         const uint32_t inv_hi = (uint32_t)((kIdxMask - q.key_off - base) >> 32);
+        // (own list: an equal high word loses on the index bits; the CTA-wide
+        // bound s.thr comes from other warps' indices, so it needs "<")
         if (!(bound & 0x1fc00000u) ||
-            (kb.seg == wl.seg && (bound | inv_hi) <= (uint32_t)(wl.thr >> 32))) {
+            (kb.seg == wl.seg && (bound | inv_hi) <= (uint32_t)(wl.thr >> 32)) ||
+            (bound | inv_hi) < (uint32_t)(s.thr[kb.seg] >> 32)) {
           const uint64_t lb = (ic.blk_lo + ic.blk_n - base) >> 7, lr = (we - base) >> 7;
           base += ((lb < lr ? lb : lr) - 1) * 128;         // + the for-increment
           continue;
