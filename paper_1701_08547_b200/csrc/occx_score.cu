@@ -772,8 +772,9 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
     // this conservative); wl_offer compares exactly.
     const uint64_t inv0 = kIdxMask - q.key_off - (sb_base + 4u * (uint32_t)lane);
     const uint32_t m = max(max(v[0], v[1]), max(v[2], v[3]));
-    const bool any = (m & 0x1fc00000u) &&
-                     (sb.seg != wl.seg || (m | (uint32_t)(inv0 >> 32)) > (uint32_t)(wl.thr >> 32));
+    const uint32_t mh = m | (uint32_t)(inv0 >> 32);
+    const bool any = (m & 0x1fc00000u) && mh >= (uint32_t)(s.thr[sb.seg] >> 32) &&
+                     (sb.seg != wl.seg || mh > (uint32_t)(wl.thr >> 32));
     if (__any_sync(0xffffffffu, any)) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -812,8 +813,9 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
     const uint64_t inv0 = kIdxMask - q.key_off - (pb + 8u * (uint32_t)lane);
     const uint32_t m = max(max(max(v[0], v[1]), max(v[2], v[3])),
                            max(max(v[4], v[5]), max(v[6], v[7])));
-    const bool any = (m & 0x1fc00000u) &&
-                     (sb.seg != wl.seg || (m | (uint32_t)(inv0 >> 32)) > (uint32_t)(wl.thr >> 32));
+    const uint32_t mh = m | (uint32_t)(inv0 >> 32);
+    const bool any = (m & 0x1fc00000u) && mh >= (uint32_t)(s.thr[sb.seg] >> 32) &&
+                     (sb.seg != wl.seg || mh > (uint32_t)(wl.thr >> 32));
     if (__any_sync(0xffffffffu, any)) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -844,8 +846,9 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
     uint32_t m = v[0];
 #pragma unroll
     for (int j = 1; j < 16; ++j) m = max(m, v[j]);
-    const bool any = (m & 0x1fc00000u) &&
-                     (sb.seg != wl.seg || (m | (uint32_t)(inv0 >> 32)) > (uint32_t)(wl.thr >> 32));
+    const uint32_t mh = m | (uint32_t)(inv0 >> 32);
+    const bool any = (m & 0x1fc00000u) && mh >= (uint32_t)(s.thr[sb.seg] >> 32) &&
+                     (sb.seg != wl.seg || mh > (uint32_t)(wl.thr >> 32));
     if (__any_sync(0xffffffffu, any)) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
