@@ -378,25 +378,21 @@ def secondary_space_api(cfg, mode: str, steps: int = 10):
     stream = torch.cuda.current_stream()
 
     def timed(prune: bool) -> float:
-        os.environ["OCCX_K2I_PRUNE"] = "1" if prune else "0"
-        try:
-            for _ in range(3):
-                plan.score_implicit(merge=False)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(steps):
-                plan.score_implicit(merge=False)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            return e0.elapsed_time(e1) / steps
-        finally:
-            os.environ.pop("OCCX_K2I_PRUNE", None)
+        for _ in range(3):
+            plan.score_implicit(merge=False, prune=prune)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            plan.score_implicit(merge=False, prune=prune)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / steps
     k_ms = timed(False)
     p_ms = timed(True)
     out = {"kernel": "score_space_kernel (K2i, implicit grid, no K3)", "kernel_ms": k_ms,
            "value": plan.total / (k_ms / 1e3), "unit": UNIT, "bound": "integer issue",
-           "note": "every candidate's key evaluated (OCCX_K2I_PRUNE=0); no candidate records "
+           "note": "every candidate's key evaluated (prune=False); no candidate records "
                    "in HBM; see profiles/r01_k2i_ncu_full.json",
            "pruned": {"kernel_ms": p_ms, "value": plan.total / (p_ms / 1e3),
                       "note": "library default: blocks skipped on an exact bound"}}
@@ -426,6 +422,41 @@ def secondary_space_api(cfg, mode: str, steps: int = 10):
 # GPU arm
 # ---------------------------------------------------------------------------
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(gpus: int) -> int:
+    """`python bench.py --gpus N` without torchrun: start the N ranks
+    ourselves (torch.distributed.run, one process per GPU, rendezvous on
+    127.0.0.1) and return their exit code.  Rank 0's JSON line goes to our
+    stdout.  NCCL communicator init is logged (NCCL_DEBUG=INFO, INIT) on
+    stderr, so the rank count of the communicator can be checked."""
+    import subprocess
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env["OCCX_BENCH_SELF_LAUNCHED"] = "1"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
+
+
+def golden_topk(workload: str, mode: str):
+    """Per-segment top-k keys recorded from the reference's functions
+    (tests/golden/make_golden.py), or None if this (config, mode) has none."""
+    path = os.path.join(ROOT, "tests", "golden", f"topk_{workload}.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(mode)
+    except OSError:
+        return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -439,18 +470,23 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=4_000_000)
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-secondary", action="store_true")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="weak: every GPU scores a full copy of the workload (default); "
-                         "strong: the GPUs split one copy")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong: the GPUs split one copy of the workload by index range "
+                         "(default; BASELINE config 5 as written); weak: every GPU scores "
+                         "its own full copy")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test harness for several ranks on one GPU")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        sys.exit(self_launch(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "ours" and world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     if args.impl == "reference":
         if rank != 0:
@@ -514,52 +550,79 @@ def main():
             return allgather_merge(local_tab.cpu(), lambda g: plan.merge(g.cuda(), g.shape[0]))
         return allgather_merge(local_tab, lambda g: plan.merge(g, g.shape[0]))
 
-    def step():
-        return gather(plan.score(records, n, index_base=key_base))
+    local_tab = torch.empty((plan.n_seg, plan.k), dtype=torch.int64, device="cuda")
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(marks=None):
+        # K2 (per-CTA partial tables) | K3 (this rank's table) | all-gather + K3
+        if marks is not None:
+            marks[0].record(stream)
+        ws = plan.score_partials(records, n, index_base=key_base)
+        if marks is not None:
+            marks[1].record(stream)
+        plan.merge(ws, plan.grid_lists, out=local_tab)
+        if marks is not None:
+            marks[2].record(stream)
+        return gather(local_tab)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    def max_over_ranks(x: float) -> float:
+    def over_ranks(x: float) -> list[float]:
+        """x from every rank (rank order)."""
         if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cpu" if gloo else "cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+            return [x]
+        t = torch.zeros(world, dtype=torch.float64, device="cpu" if gloo else "cuda")
+        t[rank] = x
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return t.cpu().tolist()
+
+    def max_over_ranks(x: float) -> float:
+        return max(over_ranks(x))
 
     sampler = ClockSampler(torch.cuda.current_device()).start()
     for _ in range(args.warmup):
         out = step()
     torch.cuda.synchronize()
     barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0, ev1 = ev(), ev()
+    marks = [[ev(), ev(), ev()] for _ in range(args.steps)]
     torch.cuda.synchronize()
     barrier()
     sampler.window_open()
     ev0.record(stream)
-    for _ in range(args.steps):
-        out = step()
+    for i in range(args.steps):
+        out = step(marks[i])
     ev1.record(stream)
     torch.cuda.synchronize()
     sampler.window_close()
     barrier()
-    ms_max = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    my_ms = ev0.elapsed_time(ev1) / args.steps
+    ms_max = max_over_ranks(my_ms)
     value = global_total / (ms_max / 1e3)
     final_keys = out.cpu().numpy().view(np.uint64)
 
-    # --- roofline: K2 alone (partials, no merge), CUDA events on the stream ---
-    reps = 10
-    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    k0.record(stream)
-    for _ in range(reps):
-        plan.score_partials(records, n, index_base=key_base)
-    k1.record(stream)
-    torch.cuda.synchronize()
-    k2_ms = k0.elapsed_time(k1) / reps
+    # --- phases of the same timed steps (events between the launches) -------
+    k2_ms = statistics.mean(m[0].elapsed_time(m[1]) for m in marks)
+    k3_ms = statistics.mean(m[1].elapsed_time(m[2]) for m in marks)
+    # all-gather + K3 after it: from the local table to the step's end
+    ends = [m[0] for m in marks[1:]] + [ev1]
+    ag_ms = statistics.mean(m[2].elapsed_time(e) for m, e in zip(marks, ends)) if world > 1 else 0.0
     hbm_peak, peak_src = _peaks()
     alg_bytes = 16 * n
     achieved = alg_bytes / (k2_ms / 1e3) / 1e9
+    k2_ranks = over_ranks(k2_ms)
+    frac_ranks = [alg_bytes / (t / 1e3) / 1e9 / hbm_peak for t in k2_ranks]
+
+    # --- parity: the merged top-k equals the reference-derived golden -------
+    golden = golden_topk(args.workload, args.mode) if args.scaling == "strong" else None
+    golden_ok = None
+    if golden is not None:
+        golden_ok = final_keys.reshape(plan.n_seg, plan.k).tolist() == golden
+        if not golden_ok:
+            raise SystemExit(f"rank {rank}: merged top-k differs from tests/golden/"
+                             f"topk_{args.workload}.json")
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
@@ -581,30 +644,26 @@ def main():
             e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
             mode = args.mode
 
-            def api_step():
+            def api_step(prune):
                 return score_space_multi(cfg.kernels, cfg.archs, mode, cfg.k,
-                                         scaling=args.scaling, gather_on_host=gloo)
+                                         scaling=args.scaling, gather_on_host=gloo,
+                                         prune=prune)
 
             def timed_api(prune: bool) -> float:
-                # OCCX_K2I_PRUNE is read by liboccx at every K2i launch
-                os.environ["OCCX_K2I_PRUNE"] = "1" if prune else "0"
-                try:
-                    for _ in range(2):
-                        api_step()
-                    torch.cuda.synchronize()
-                    barrier()
-                    e0 = torch.cuda.Event(enable_timing=True)
-                    e1 = torch.cuda.Event(enable_timing=True)
-                    e0.record(stream)
-                    for _ in range(e2e_steps):
-                        segs, keys = api_step()
-                    e1.record(stream)
-                    torch.cuda.synchronize()
-                    assert np.array_equal(keys.numpy().view(np.uint64), final_keys), \
-                        "API top-k differs from the record path"
-                    return max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
-                finally:
-                    os.environ.pop("OCCX_K2I_PRUNE", None)
+                for _ in range(2):
+                    api_step(prune)
+                torch.cuda.synchronize()
+                barrier()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(e2e_steps):
+                    segs, keys = api_step(prune)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                assert np.array_equal(keys.numpy().view(np.uint64), final_keys), \
+                    "API top-k differs from the record path"
+                return max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
             # headline: every candidate's key evaluated (block pruning off)
             e_ms = timed_api(prune=False)
             p_ms = timed_api(prune=True)
@@ -674,6 +733,8 @@ def main():
         except Exception as exc:
             c_oracle = {"error": repr(exc)[:200]}
 
+    if world > 1:
+        barrier()
     if rank == 0:
         # K2 + K3 per step, + K3 after the all-gather for N > 1
         launches = args.steps * (2 + (1 if world > 1 else 0))
@@ -696,11 +757,20 @@ def main():
                          "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                          "kernel": "score_topk_kernel (K2)", "kernel_ms": k2_ms,
                          "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src,
-                         "note": "peak is the driver's copy (read+write) bandwidth; K2 only "
-                                 "reads its 16-B records, and a read stream can exceed the copy "
-                                 "figure (ncu dram__bytes_read per launch is in traffic)"},
+                         "frac_per_rank": frac_ranks, "kernel_ms_per_rank": k2_ranks,
+                         "note": "K2 time from CUDA events around its launch inside the timed "
+                                 "steps; peak is the driver's copy (read+write) bandwidth; K2 "
+                                 "only reads its 16-B records, and a read stream can exceed the "
+                                 "copy figure (ncu dram__bytes_read per launch is in traffic)"},
+            "phases_ms": {"k2_score": k2_ms, "k3_local_merge": k3_ms,
+                          "allgather_and_k3": ag_ms, "step": my_ms,
+                          "note": "rank 0, mean over the timed steps (CUDA events between "
+                                  "the launches); allgather_and_k3 is 0 at N = 1"},
+            "topk_equals_golden": golden_ok,
             "e2e": e2e, "gpu_launches": launches, "clocks": sampler.summary(),
         }
+        if os.environ.get("OCCX_BENCH_SELF_LAUNCHED"):
+            line["launch"] = "self-launched: torch.distributed.run, one rank per GPU"
         if e2e_records is not None:
             line["e2e_records"] = e2e_records
         if secondary is not None:

@@ -16,8 +16,10 @@
  *    valid once the stream is synchronised.
  *  - Return value is an occx_status; codes map 1:1 onto the reference's
  *    exception classes (pkg/src/occmix/errors.py:4-48).
- *  - A context caches device properties only (SM count, smem limit); it is
- *    immutable after create and safe to share across threads and streams.
+ *  - A context caches device properties (SM count, smem limit) and the
+ *    options it was created with; it is immutable after create and safe to
+ *    share across threads and streams.  The library reads no environment
+ *    variables.
  */
 #ifndef OCCX_H
 #define OCCX_H
@@ -29,7 +31,7 @@
 extern "C" {
 #endif
 
-#define OCCX_ABI_VERSION 1
+#define OCCX_ABI_VERSION 2
 #define OCCX_MAX_K 32          /* top-k list length limit                     */
 #define OCCX_MAX_ARCHS 32      /* archs per launch (u8 index, param block)    */
 #define OCCX_N_CLASSES 15      /* 14 countable OpClass rows + Unclassified    */
@@ -52,6 +54,17 @@ typedef enum occx_status {
 } occx_status;
 
 typedef enum occx_mode { OCCX_MODE_CORRECTED = 0, OCCX_MODE_VERBATIM = 1 } occx_mode;
+
+/* Context options (occx_ctx_create_ex).  They pick among implementations
+ * with identical results: K2 fed by 128-bit LDG instead of the TMA ring
+ * (two 512-thread CTAs per SM; the workspace doubles), or the TMA ring with
+ * one slice per warp per stage.  Default 0: TMA, two slices.             */
+#define OCCX_CTX_K2_FEED_LDG 0x1u
+#define OCCX_CTX_K2_ONE_SLICE 0x2u
+
+/* occx_score_space flags.  EVERY_KEY: evaluate every candidate's key (no
+ * block-bound pruning); the top-k is the same either way.               */
+#define OCCX_SCORE_EVERY_KEY 0x1u
 typedef enum occx_sum_mode {
   OCCX_SUM_NEUMAIER = 0,   /* CPython >= 3.12 float sum()                     */
   OCCX_SUM_NAIVE = 1       /* CPython <= 3.11 float sum()                     */
@@ -170,7 +183,9 @@ typedef struct occx_ctx occx_ctx;
 /* ---- library / context ------------------------------------------------ */
 int occx_abi_version(void);
 const char* occx_status_string(int status);
-int occx_ctx_create(int device, occx_ctx** out);
+int occx_ctx_create(int device, occx_ctx** out);          /* options 0 */
+int occx_ctx_create_ex(int device, uint32_t options, occx_ctx** out);
+uint32_t occx_ctx_options(const occx_ctx* ctx);
 int occx_ctx_destroy(occx_ctx* ctx);
 int occx_ctx_sm_count(const occx_ctx* ctx);
 /* Host-side check that h_archs fit the device tables; *bad = first failing
@@ -255,11 +270,13 @@ int occx_topk_merge(const occx_ctx* ctx, const uint64_t* d_lists,
  * Segment blocks (|REGS| x |SMEM|) must be < 2^32 candidates.
  * key_offset is added to every candidate's global index in its key (0 for
  * the plain space; r * total when rank r of a weak-scaling run scores its
- * own copy of the space, so keys stay unique across ranks).             */
+ * own copy of the space, so keys stay unique across ranks).  flags: 0 or
+ * OCCX_SCORE_EVERY_KEY (same top-k; no block skipping).                  */
 int occx_score_space(const occx_ctx* ctx, const occx_arch_t* h_archs, int n_arch,
                      const occx_segdesc_t* d_desc, uint32_t n_desc,
                      const uint32_t* d_pool, uint32_t n_pool, uint64_t begin,
-                     uint64_t n, uint64_t key_offset, int mode, const occx_vent_t* d_vtab, uint32_t n_var,
+                     uint64_t n, uint64_t key_offset, int mode, uint32_t flags,
+                     const occx_vent_t* d_vtab, uint32_t n_var,
                      uint32_t n_seg, uint32_t k, void* d_ws, uint64_t ws_bytes,
                      uint64_t* d_topk, void* stream);
 
@@ -282,6 +299,10 @@ int occx_gen_space(const occx_ctx* ctx, const occx_segdesc_t* d_desc,
  * occx_sass_free (also call it after errors).                           */
 typedef struct occx_sass occx_sass;
 int occx_sass_parse(const char* utf8, uint64_t n_bytes, occx_sass** out, int64_t* err_line);
+/* Same, with the minimum bytes per worker-thread chunk (0 = 4 MB default);
+ * small values split the text at many line boundaries (results identical). */
+int occx_sass_parse_ex(const char* utf8, uint64_t n_bytes, uint64_t chunk_bytes_min,
+                       occx_sass** out, int64_t* err_line);
 uint32_t occx_sass_n_kernels(const occx_sass* r);
 uint64_t occx_sass_n_instr(const occx_sass* r);
 const uint32_t* occx_sass_records(const occx_sass* r);

@@ -16,8 +16,37 @@ interpreter's builtin ``sum()``, exactly as the reference does.
 
 from __future__ import annotations
 
+import contextlib
+import functools
 import heapq
 import math
+import operator
+
+# CPython's builtin float sum() is Neumaier-compensated from 3.12 on and a
+# plain left-to-right loop before (Objects/bltinmodule.c builtin_sum_impl:
+# int start 0, then ``f_result += item`` per float).  The reference sums its
+# float terms with builtin sum() (mix.py:278, :330, :349), so its bits depend
+# on the interpreter; _fsum is the summation every float sum below uses:
+# builtin sum() by default, or the <= 3.11 loop under sum_semantics("naive").
+_fsum = sum
+
+
+def naive_sum(values):
+    """CPython <= 3.11 float sum(): ((0 + x0) + x1) + ... left to right."""
+    return functools.reduce(operator.add, values, 0)
+
+
+@contextlib.contextmanager
+def sum_semantics(which):
+    """Restate the reference under another interpreter's sum():
+    "naive" (CPython <= 3.11) or "builtin" (this interpreter)."""
+    global _fsum
+    old = _fsum
+    _fsum = {"naive": naive_sum, "builtin": sum}[which]
+    try:
+        yield
+    finally:
+        _fsum = old
 
 
 class OracleIllegalLaunch(Exception):
@@ -221,8 +250,8 @@ def _flops_coefficient(counts, col):      # mix.py:268-281
     total = flops(counts)
     if total == 0:
         return cpi("FPIns32", col)
-    weighted = sum(n * cpi(c, col) for c, n in counts.items()
-                   if CATEGORY.get(c) == "FLOPS")
+    weighted = _fsum([n * cpi(c, col) for c, n in counts.items()
+                      if CATEGORY.get(c) == "FLOPS"])
     return weighted / total
 
 
@@ -237,7 +266,7 @@ def category_cycles(counts, reg_operands, cc):   # mix.py:284-306
 def cost_estimate(counts, reg_operands, cc, scale=1.0):   # mix.py:321-330
     if scale <= 0:
         raise ValueError("scale must be positive")
-    return scale * sum(category_cycles(counts, reg_operands, cc).values())
+    return scale * _fsum(list(category_cycles(counts, reg_operands, cc).values()))
 
 
 def intensity(counts):                    # mix.py:333-337
@@ -249,7 +278,7 @@ def intensity(counts):                    # mix.py:333-337
 
 def pipeline_utilization(counts, reg_operands, cc):   # mix.py:340-352
     cyc = category_cycles(counts, reg_operands, cc)
-    total = sum(cyc.values())
+    total = _fsum(list(cyc.values()))
     if total == 0:
         return {k: 0.0 for k in cyc}
     return {k: v / total for k, v in cyc.items()}

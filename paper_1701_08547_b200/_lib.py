@@ -55,6 +55,8 @@ SIGNATURES = {
     "occx_abi_version": ([], _I),
     "occx_status_string": ([_I], ctypes.c_char_p),
     "occx_ctx_create": ([_I, _P], _I),
+    "occx_ctx_create_ex": ([_I, _U32, _P], _I),
+    "occx_ctx_options": ([_P], _U32),
     "occx_ctx_destroy": ([_P], _I),
     "occx_ctx_sm_count": ([_P], _I),
     "occx_check_archs": ([_P, _I, _P], _I),
@@ -69,6 +71,7 @@ SIGNATURES = {
     "occx_topk_merge": ([_P, _P, _U32, _U32, _U32, _P, _P], _I),
     "occx_gen_space": ([_P, _P, _U32, _P, _U64, _U64, _P, _P], _I),
     "occx_sass_parse": ([ctypes.c_char_p, _U64, _P, _P], _I),
+    "occx_sass_parse_ex": ([ctypes.c_char_p, _U64, _U64, _P, _P], _I),
     "occx_sass_n_kernels": ([_P], _U32),
     "occx_sass_n_instr": ([_P], _U64),
     "occx_sass_records": ([_P], _P),
@@ -78,9 +81,8 @@ SIGNATURES = {
     "occx_sass_signature": ([_P, _U32], ctypes.c_char_p),
     "occx_sass_error_text": ([_P], ctypes.c_char_p),
     "occx_sass_free": ([_P], None),
-    "occx_score_space": ([_P, _P, _I, _P, _U32, _P, _U32, _U64, _U64, _U64, _I, _P, _U32, _U32,
-                          _U32,
-                          _P, _U64, _P, _P], _I),
+    "occx_score_space": ([_P, _P, _I, _P, _U32, _P, _U32, _U64, _U64, _U64, _I, _U32, _P, _U32,
+                          _U32, _U32, _P, _U64, _P, _P], _I),
 }
 
 
@@ -121,22 +123,27 @@ def check(status: int, what: str) -> None:
         raise_status(status, f"{what}: {msg}")
 
 
-_ctx: dict[int, int] = {}
+# context options (include/occx.h): implementation choices, same results
+CTX_K2_FEED_LDG = 0x1
+CTX_K2_ONE_SLICE = 0x2
+SCORE_EVERY_KEY = 0x1           # occx_score_space flag: no block-bound pruning
+
+_ctx: dict[tuple[int, int], int] = {}
 
 
-def ctx(device: int | None = None) -> int:
-    """Per-device context handle (created once, immutable)."""
+def ctx(device: int | None = None, options: int = 0) -> int:
+    """Per-(device, options) context handle (created once, immutable)."""
     import torch
     if not _ctx and not torch.cuda.is_available():
         raise DeviceError("no CUDA device: the occx backend runs on the GPU only")
     dev = torch.cuda.current_device() if device is None else device
     with _lock:
-        h = _ctx.get(dev)
+        h = _ctx.get((dev, options))
     if h is None:
         out = ctypes.c_void_p()
-        check(load().occx_ctx_create(dev, ctypes.byref(out)), "occx_ctx_create")
+        check(load().occx_ctx_create_ex(dev, options, ctypes.byref(out)), "occx_ctx_create_ex")
         with _lock:
-            h = _ctx.setdefault(dev, out.value)
+            h = _ctx.setdefault((dev, options), out.value)
         if h != out.value:          # another thread won the race: drop ours
             load().occx_ctx_destroy(out)
     return h

@@ -487,9 +487,13 @@ class ScorePlan:
 
     def __init__(self, kernels: Sequence[KernelSpec], archs: Sequence[ArchSpec],
                  mode: Mode = Mode.CORRECTED, k: int = 16,
-                 table: ThroughputTable = DEFAULT_THROUGHPUT, scale: float = 1.0):
+                 table: ThroughputTable = DEFAULT_THROUGHPUT, scale: float = 1.0,
+                 options: int = 0):
+        """``options``: occx context options (_lib.CTX_*), implementation
+        choices of the record scorer with identical results."""
         if not 1 <= k <= 32:
             raise ValueError("k must be in [1, 32]")
+        self._ctx = _lib.ctx(options=options)
         self.kernels = list(kernels)
         self.archs = list(archs)
         self.mode = Mode(mode)
@@ -596,9 +600,11 @@ class ScorePlan:
             _lib.ptr(self.d_var_kernel), _lib.ptr(self.d_masks),
             _lib.ptr(self.d_vtab), _lib.stream_ptr()), "occx_build_vtab")
         ws = ctypes_u64()
-        _lib.check(_lib.load().occx_score_workspace_bytes(_lib.ctx(), self.n_seg, k,
+        _lib.check(_lib.load().occx_score_workspace_bytes(self._ctx, self.n_seg, k,
                                                           ws.ref()), "workspace")
         self.ws_bytes = ws.value
+        # per-CTA partial tables K2 leaves in the workspace (score_partials)
+        self.grid_lists = self.ws_bytes // (self.n_seg * k * 8)
         self.d_ws = _empty(self.ws_bytes)
         self.masks = masks
 
@@ -608,7 +614,7 @@ class ScorePlan:
         n = self.total - begin if n is None else n
         out = out if out is not None else _empty(n * 16)
         _lib.check(_lib.load().occx_gen_space(
-            _lib.ctx(), _lib.ptr(self.d_desc), self.n_seg, _lib.ptr(self.d_pool), begin, n,
+            self._ctx, _lib.ptr(self.d_desc), self.n_seg, _lib.ptr(self.d_pool), begin, n,
             _lib.ptr(out), _lib.stream_ptr()), "occx_gen_space")
         return out
 
@@ -624,7 +630,7 @@ class ScorePlan:
         out = out if out is not None else torch.empty((self.n_seg, self.k), dtype=torch.int64,
                                                       device="cuda")
         _lib.check(_lib.load().occx_score_topk(
-            _lib.ctx(), _lib.ptr(self.h_archs), self.n_arch, _lib.ptr(d_records), n, index_base,
+            self._ctx, _lib.ptr(self.h_archs), self.n_arch, _lib.ptr(d_records), n, index_base,
             MODE_CODE[self.mode], _lib.ptr(self.d_vtab), self.n_var, self.n_seg, self.k,
             _lib.ptr(self.d_ws), self.ws_bytes, _lib.ptr(out), _lib.stream_ptr(stream)),
             "occx_score_topk")
@@ -633,7 +639,7 @@ class ScorePlan:
     def score_partials(self, d_records, n: int, index_base: int = 0, stream=None):
         """K2 only: per-CTA tables left in the workspace (timing / custom merges)."""
         _lib.check(_lib.load().occx_score_topk(
-            _lib.ctx(), _lib.ptr(self.h_archs), self.n_arch, _lib.ptr(d_records), n, index_base,
+            self._ctx, _lib.ptr(self.h_archs), self.n_arch, _lib.ptr(d_records), n, index_base,
             MODE_CODE[self.mode], _lib.ptr(self.d_vtab), self.n_var, self.n_seg, self.k,
             _lib.ptr(self.d_ws), self.ws_bytes, None, _lib.stream_ptr(stream)),
             "occx_score_topk")
@@ -672,19 +678,21 @@ class ScorePlan:
         return self.merge(tables, n_chunks)
 
     def score_implicit(self, begin: int = 0, n: int | None = None, out=None, stream=None,
-                       merge: bool = True, key_offset: int = 0):
+                       merge: bool = True, key_offset: int = 0, prune: bool = True):
         """K2i: score candidates [begin, begin+n) of the space decoded from their
         global index inside the kernel (no records in HBM).  Identical keys to
         generate() + score(); returns the device [n_seg, k] table.
         ``key_offset`` shifts the index carried in the keys (a weak-scaling
-        rank scoring its own copy of the space)."""
+        rank scoring its own copy of the space).  ``prune=False`` evaluates
+        every candidate's key (no exact block-bound skipping; same top-k)."""
         torch = _torch()
         n = self.total - begin if n is None else n
         if merge and out is None:
             out = torch.empty((self.n_seg, self.k), dtype=torch.int64, device="cuda")
         _lib.check(_lib.load().occx_score_space(
-            _lib.ctx(), _lib.ptr(self.h_archs), self.n_arch, _lib.ptr(self.d_desc), self.n_seg,
+            self._ctx, _lib.ptr(self.h_archs), self.n_arch, _lib.ptr(self.d_desc), self.n_seg,
             _lib.ptr(self.d_pool), self.n_pool, begin, n, key_offset, MODE_CODE[self.mode],
+            0 if prune else _lib.SCORE_EVERY_KEY,
             _lib.ptr(self.d_vtab), self.n_var, self.n_seg, self.k, _lib.ptr(self.d_ws),
             self.ws_bytes, _lib.ptr(out) if merge else None, _lib.stream_ptr(stream)),
             "occx_score_space")
@@ -696,7 +704,7 @@ class ScorePlan:
         out = out if out is not None else torch.empty((self.n_seg, self.k), dtype=torch.int64,
                                                       device="cuda")
         _lib.check(_lib.load().occx_topk_merge(
-            _lib.ctx(), _lib.ptr(d_lists), n_lists, self.n_seg, self.k, _lib.ptr(out),
+            self._ctx, _lib.ptr(d_lists), n_lists, self.n_seg, self.k, _lib.ptr(out),
             _lib.stream_ptr(stream)), "occx_topk_merge")
         return out
 
@@ -791,12 +799,14 @@ class ctypes_u64:
 
 
 def score_space(kernels: Sequence[KernelSpec], archs: Sequence[ArchSpec],
-                mode: Mode = Mode.CORRECTED, k: int = 16) -> list[SegmentTopK]:
+                mode: Mode = Mode.CORRECTED, k: int = 16,
+                prune: bool = True) -> list[SegmentTopK]:
     """Score every candidate of the kernels' spaces on every arch; return
     the top-k configurations per (kernel, arch).  Candidates are decoded
     from their index inside the scorer (K2i): nothing but the space
-    description, the feature table and the top-k table touch HBM."""
+    description, the feature table and the top-k table touch HBM.
+    ``prune=False`` evaluates every key (no exact block skipping)."""
     plan = ScorePlan(kernels, archs, mode, k)
-    keys = plan.score_implicit()
+    keys = plan.score_implicit(prune=prune)
     plan.decode_tables()               # host work while the GPU scores
     return plan.decode(keys)

@@ -38,32 +38,36 @@ def _stale(obj: str, deps: list[str]) -> bool:
 
 
 def build(verbose: bool = False) -> str:
+    """Compile the stale sources (in parallel) and link liboccx.so."""
     os.makedirs(BUILD, exist_ok=True)
-    header_deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
+    header_deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)
+                   if f.endswith((".cuh", ".h"))]
     header_deps += [os.path.join(os.path.dirname(HERE), "include", "occx.h"), __file__]
-    objs = []
+    objs, jobs = [], []
     for src, extra in SOURCES.items():
         path = os.path.join(CSRC, src)
         obj = os.path.join(BUILD, src.replace(".cu", ".o"))
         objs.append(obj)
         if _stale(obj, [path] + header_deps):
-            cmd = [NVCC, *ARCH, *COMMON, *extra, "-c", path, "-o", obj]
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            if verbose or r.returncode:
-                sys.stderr.write(r.stdout + r.stderr)
-            if r.returncode:
-                raise RuntimeError(f"nvcc failed on {src}")
+            jobs.append((src, [NVCC, *ARCH, *COMMON, *extra, "-c", path, "-o", obj]))
     for src, extra in CXX_SOURCES.items():
         path = os.path.join(CSRC, src)
         obj = os.path.join(BUILD, src.replace(".cpp", ".o"))
         objs.append(obj)
         if _stale(obj, [path] + header_deps):
-            cmd = [CXX, "-O3", "-std=c++17", "-fPIC", "-Wall", "-c", path, "-o", obj, *extra]
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            if verbose or r.returncode:
-                sys.stderr.write(r.stdout + r.stderr)
-            if r.returncode:
-                raise RuntimeError(f"c++ failed on {src}")
+            jobs.append((src, [CXX, "-O3", "-std=c++17", "-fPIC", "-Wall", "-c", path,
+                               "-o", obj, *extra]))
+    procs = [(src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
+                                    text=True)) for src, cmd in jobs]
+    failed = []
+    for src, pr in procs:
+        out, _ = pr.communicate()
+        if verbose or pr.returncode:
+            sys.stderr.write(out)
+        if pr.returncode:
+            failed.append(src)
+    if failed:
+        raise RuntimeError(f"compile failed on {', '.join(failed)}")
     if _stale(OUT, objs):
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", OUT, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -17,13 +17,21 @@ extern "C" const char* occx_status_string(int status) {
     case OCCX_ERR_CAPACITY: return "input exceeds a device table limit";
     case OCCX_ERR_KEY: return "missing throughput-table entry (KeyError)";
     case OCCX_ERR_INDEX: return "empty thread-candidate list (IndexError)";
+    case OCCX_ERR_PARSE: return "unparseable input line (ParseError)";
+    case OCCX_ERR_EMPTY: return "input has no instructions (EmptyInputError)";
+    case OCCX_ERR_ATTRIBUTE: return "reference parser AttributeError (sass.py:278-279 quirk)";
     default: return "unknown status";
   }
 }
 
 extern "C" int occx_ctx_create(int device, occx_ctx** out) {
+  return occx_ctx_create_ex(device, 0u, out);
+}
+
+extern "C" int occx_ctx_create_ex(int device, uint32_t options, occx_ctx** out) {
   if (!out) return OCCX_ERR_VALUE;
   *out = nullptr;
+  if (options & ~(uint32_t)(OCCX_CTX_K2_FEED_LDG | OCCX_CTX_K2_ONE_SLICE)) return OCCX_ERR_VALUE;
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) return OCCX_ERR_CUDA;
   cudaDeviceProp prop;
@@ -35,6 +43,7 @@ extern "C" int occx_ctx_create(int device, occx_ctx** out) {
   c->max_smem_optin = (int)prop.sharedMemPerBlockOptin;
   c->cc_major = prop.major;
   c->cc_minor = prop.minor;
+  c->options = options;
   *out = c;
   return OCCX_OK;
 }
@@ -45,3 +54,5 @@ extern "C" int occx_ctx_destroy(occx_ctx* ctx) {
 }
 
 extern "C" int occx_ctx_sm_count(const occx_ctx* ctx) { return ctx ? ctx->sm_count : 0; }
+
+extern "C" uint32_t occx_ctx_options(const occx_ctx* ctx) { return ctx ? ctx->options : 0u; }

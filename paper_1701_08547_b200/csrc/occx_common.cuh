@@ -262,4 +262,5 @@ struct occx_ctx {
   int sm_count;
   int max_smem_optin;
   int cc_major, cc_minor;
+  uint32_t options;      // OCCX_CTX_* bits, fixed at create (include/occx.h)
 };

@@ -493,6 +493,11 @@ struct occx_sass {
 
 extern "C" int occx_sass_parse(const char* text, uint64_t n_bytes, occx_sass** out,
                                int64_t* err_line) {
+  return occx_sass_parse_ex(text, n_bytes, 0, out, err_line);
+}
+
+extern "C" int occx_sass_parse_ex(const char* text, uint64_t n_bytes, uint64_t chunk_bytes_min,
+                                  occx_sass** out, int64_t* err_line) {
   if (!out) return OCCX_ERR_VALUE;
   occx_sass* r = new occx_sass();
   *out = r;
@@ -501,11 +506,8 @@ extern "C" int occx_sass_parse(const char* text, uint64_t n_bytes, occx_sass** o
   // line-aligned chunks (cut after '\n'; a "\r\n" pair never straddles a cut)
   unsigned hw = std::thread::hardware_concurrency();
   const unsigned max_t = hw ? (hw < 32 ? hw : 32) : 1;
-  uint64_t chunk_bytes = 4u << 20;                             // >= 4 MB per chunk
-  if (const char* e = std::getenv("OCCX_SASS_CHUNK_BYTES")) {  // test hook: force small chunks
-    const long long v = std::atoll(e);
-    if (v > 0) chunk_bytes = (uint64_t)v;
-  }
+  // >= 4 MB per chunk by default; callers (tests) may force small chunks
+  const uint64_t chunk_bytes = chunk_bytes_min ? chunk_bytes_min : (uint64_t)(4u << 20);
   unsigned n_chunks = (unsigned)(n_bytes / chunk_bytes) + 1;
   if (n_chunks > max_t) n_chunks = max_t;
   std::vector<size_t> cut{0};

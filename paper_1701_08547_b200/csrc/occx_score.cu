@@ -1429,14 +1429,14 @@ extern "C" int occx_occupancy_batch(const occx_ctx* ctx, const occx_arch_t* h_ar
 
 enum { kFeedTma = 0, kFeedLdg = 1 };
 
-static int score_feed() {
-  const char* e = std::getenv("OCCX_K2_FEED");      // A/B switch for benchmarking
-  return (e && e[0] == 'l') ? kFeedLdg : kFeedTma;
+static int score_feed(const occx_ctx* ctx) {
+  // fixed per context (occx_ctx_create_ex options): the workspace size follows it
+  return (ctx->options & OCCX_CTX_K2_FEED_LDG) ? kFeedLdg : kFeedTma;
 }
 
 static int score_grid(const occx_ctx* ctx) {
   // persistent: TMA feed one 544-thread CTA per SM; LDG feed two 512-thread CTAs
-  return score_feed() == kFeedTma ? ctx->sm_count : ctx->sm_count * 2;
+  return score_feed(ctx) == kFeedTma ? ctx->sm_count : ctx->sm_count * 2;
 }
 
 extern "C" int occx_score_workspace_bytes(const occx_ctx* ctx, uint32_t n_seg, uint32_t k,
@@ -1481,14 +1481,14 @@ extern "C" int occx_score_topk(const occx_ctx* ctx, const occx_arch_t* h_archs, 
   p.k = k;
   p.partials = static_cast<uint64_t*>(d_ws);
   const int grid = score_grid(ctx);
-  const int feed = score_feed();
+  const int feed = score_feed(ctx);
   p.vt_smem = ((uint64_t)n_var * n_arch <= (uint64_t)kVtSmemMax) ? 1u : 0u;
   size_t smem = k2_tail_bytes(p.archs, n_var, n_seg, k, p.vt_smem != 0);
   // two slices per warp (64 KB stages, 192 KB in flight per SM) whenever the
   // ring fits: per-SM bandwidth is bytes-in-flight bound (config 2: 0.123 ->
-  // 0.107 ms, config 4: 0.309 -> 0.298 ms vs one slice).  OCCX_K2_SL=1 forces one.
-  const char* sl_env = std::getenv("OCCX_K2_SL");
-  const bool one_slice = sl_env && sl_env[0] == '1';
+  // 0.107 ms, config 4: 0.309 -> 0.298 ms vs one slice).  OCCX_CTX_K2_ONE_SLICE
+  // (context option) forces one.
+  const bool one_slice = (ctx->options & OCCX_CTX_K2_ONE_SLICE) != 0;
   int sl = (feed == kFeedTma && !one_slice &&
             smem + TmaRing<2>::kBytes + 2 * TmaRing<2>::kStages * 8 <= (size_t)ctx->max_smem_optin)
                ? 2 : 1;
@@ -1592,12 +1592,13 @@ extern "C" int occx_gen_space(const occx_ctx* ctx, const occx_segdesc_t* d_desc,
 extern "C" int occx_score_space(const occx_ctx* ctx, const occx_arch_t* h_archs, int n_arch,
                                 const occx_segdesc_t* d_desc, uint32_t n_desc,
                                 const uint32_t* d_pool, uint32_t n_pool, uint64_t begin,
-                                uint64_t n, uint64_t key_offset, int mode,
+                                uint64_t n, uint64_t key_offset, int mode, uint32_t flags,
                                 const occx_vent_t* d_vtab, uint32_t n_var,
                                 uint32_t n_seg, uint32_t k, void* d_ws, uint64_t ws_bytes,
                                 uint64_t* d_topk, void* stream) {
   if (!ctx || (mode != 0 && mode != 1) || k == 0 || k > OCCX_MAX_K || n_seg == 0 ||
-      n_desc == 0 || d_desc == nullptr || d_pool == nullptr)
+      n_desc == 0 || d_desc == nullptr || d_pool == nullptr ||
+      (flags & ~(uint32_t)OCCX_SCORE_EVERY_KEY) != 0)
     return OCCX_ERR_VALUE;
   int bad;
   int st = occx_check_archs(h_archs, n_arch, &bad);
@@ -1634,8 +1635,7 @@ extern "C" int occx_score_space(const occx_ctx* ctx, const occx_arch_t* h_archs,
   if (smem > (size_t)ctx->max_smem_optin) return OCCX_ERR_CAPACITY;
   // per-warp separable tables when they fit (else the general path only)
   q.sep_words = smem + (size_t)kIgWarps * kIgTab * 4 <= (size_t)ctx->max_smem_optin ? kIgTab : 0;
-  const char* pr = std::getenv("OCCX_K2I_PRUNE");      // 0: score every candidate
-  q.prune = (pr && pr[0] == '0') ? 0u : 1u;
+  q.prune = (flags & OCCX_SCORE_EVERY_KEY) ? 0u : 1u;    // exact block-bound pruning
   smem += (size_t)kIgWarps * q.sep_words * 4;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
 #define OCCX_LAUNCH_IG(KERNEL)                                                       \

@@ -44,7 +44,8 @@ def allgather_merge(local_table, merge: Callable, group=None):
 
 
 def score_space_multi(kernels, archs, mode="corrected", k: int = 16, group=None,
-                      scaling: str = "strong", gather_on_host: bool = False):
+                      scaling: str = "strong", gather_on_host: bool = False,
+                      prune: bool = True):
     """The multi-GPU form of ``score_space()`` (the public API a user calls on
     every rank): build the plan from the host-side space description (its
     tables go H2D), score on the device with K2i, all-gather + K3 merge the
@@ -54,17 +55,18 @@ def score_space_multi(kernels, archs, mode="corrected", k: int = 16, group=None,
     ``scaling="strong"``: the ranks split one space by index range.
     ``scaling="weak"``: every rank scores its own copy of the space; copy r
     carries global indices [r*total, (r+1)*total) so keys stay unique.
-    ``gather_on_host``: all-gather host tensors (gloo transport)."""
+    ``gather_on_host``: all-gather host tensors (gloo transport).
+    ``prune=False``: evaluate every candidate's key (same result)."""
     import torch.distributed as dist
     from .batch import ScorePlan
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     plan = ScorePlan(kernels, archs, mode, k)
     if scaling == "weak":
-        local = plan.score_implicit(0, plan.total, key_offset=rank * plan.total)
+        local = plan.score_implicit(0, plan.total, key_offset=rank * plan.total, prune=prune)
     elif scaling == "strong":
         begin, end = shard_range(plan.total, rank, world)
-        local = plan.score_implicit(begin, end - begin)
+        local = plan.score_implicit(begin, end - begin, prune=prune)
     else:
         raise ValueError("scaling must be 'strong' or 'weak'")
     plan.decode_tables()               # host work while the GPU scores

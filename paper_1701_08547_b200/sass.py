@@ -35,12 +35,15 @@ class SassRecords:
         return np.asarray(lut or [DEVICE_ID[OpClass.UNCLASSIFIED]], np.uint8)
 
 
-def tokenize(text: str) -> SassRecords:
+def tokenize(text: str, chunk_bytes: int = 0) -> SassRecords:
+    """``chunk_bytes``: minimum bytes per worker-thread chunk (0 = library
+    default); only the split changes, never the result."""
     lib = _lib.load()
     data = text.encode("utf-8", "surrogatepass")
     h = ctypes.c_void_p()
     line = ctypes.c_int64(0)
-    st = lib.occx_sass_parse(data, len(data), ctypes.byref(h), ctypes.byref(line))
+    st = lib.occx_sass_parse_ex(data, len(data), int(chunk_bytes), ctypes.byref(h),
+                                ctypes.byref(line))
     try:
         if st:
             err = lib.occx_sass_error_text(h).decode("utf-8", "surrogatepass")

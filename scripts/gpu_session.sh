@@ -15,5 +15,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:score_topk -s 3 -c 1 -f \
   -o $OUT/k2_full_$TAG python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --no-secondary > /dev/null 2>&1; echo "ncu k2 rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:score_space_kernel -s 28 -c 1 -f \
-  -o $OUT/k2i_full_$TAG env OCCX_K2I_PRUNE=0 python scripts/k2i_bench.py > /dev/null 2>&1; echo "ncu k2i rc=$?"
+  -o $OUT/k2i_full_$TAG python scripts/k2i_bench.py --every-key > /dev/null 2>&1; echo "ncu k2i rc=$?"
 ls -la $OUT

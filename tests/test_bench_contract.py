@@ -27,7 +27,50 @@ def test_reference_arm_line():
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
-    assert d["higher_is_better"] is True and d["scaling"] == "weak"
+    assert d["higher_is_better"] is True and d["scaling"] == "strong"
+
+
+def test_self_launch_command(monkeypatch):
+    """`bench.py --gpus N` outside torchrun starts N ranks itself (one per
+    GPU, rendezvous on 127.0.0.1) with NCCL init logging on."""
+    import bench
+    seen = {}
+
+    class R:
+        returncode = 0
+
+    def fake_run(cmd, env):
+        seen["cmd"], seen["env"] = cmd, env
+        return R()
+    monkeypatch.setattr(subprocess, "run", fake_run)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "5"])
+    assert bench.self_launch(4) == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "5"] and cmd[-5].endswith("bench.py")
+    assert seen["env"]["NCCL_DEBUG"] and seen["env"]["OCCX_BENCH_SELF_LAUNCHED"] == "1"
+
+
+def test_world_size_must_match_gpus():
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "4"], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode != 0 and "--gpus 4 but WORLD_SIZE=2" in r.stderr
+
+
+@pytest.mark.gpu
+def test_self_launched_two_ranks_strong_golden():
+    """No torchrun: bench.py launches its 2 ranks itself (gloo harness on the
+    one GPU), splits config 2 by index range and checks the merged top-k
+    against tests/golden/topk_config2.json on every rank."""
+    d = _run(["bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3", "--dist-backend",
+              "gloo", "--workload", "config2", "--no-cpu", "--no-secondary"], timeout=900)
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong"
+    assert d["launch"].startswith("self-launched")
+    assert d["topk_equals_golden"] is True
+    assert d["config"]["candidates"] == 26_214_400
+    assert d["phases_ms"]["allgather_and_k3"] > 0 and len(d["roofline"]["frac_per_rank"]) == 2
 
 
 @pytest.mark.gpu

@@ -24,10 +24,32 @@ def test_exports_every_header_function(lib):
 
 
 def test_abi_version_and_status_strings(lib):
-    assert lib.occx_abi_version() == 1
-    for code in range(11):
-        assert lib.occx_status_string(code)
+    assert lib.occx_abi_version() == 2
+    for code in range(14):
+        assert lib.occx_status_string(code) != b"unknown status", code
+    assert lib.occx_status_string(14) == b"unknown status"
     assert b"IllegalLaunchError" in lib.occx_status_string(2)
+    assert b"ParseError" in lib.occx_status_string(11)
+    assert b"EmptyInputError" in lib.occx_status_string(12)
+    assert b"AttributeError" in lib.occx_status_string(13)
+
+
+def test_ctx_options_validated_before_device(lib):
+    out = ctypes.c_void_p()
+    assert lib.occx_ctx_create_ex(0, 0x4, ctypes.byref(out)) == 1       # unknown option bit
+    assert lib.occx_ctx_create_ex(0, 0, None) == 1
+    assert lib.occx_ctx_options(None) == 0
+
+
+def test_library_reads_no_environment():
+    """Implementation switches are explicit arguments (ctx options, score
+    flags, tokenizer chunk size), not environment variables."""
+    import os
+    import re
+    csrc = os.path.join(os.path.dirname(_lib.__file__), "csrc")
+    for f in os.listdir(csrc):
+        text = open(os.path.join(csrc, f), encoding="utf-8").read()
+        assert not re.search(r"\bgetenv\s*\(", text), f
 
 
 def test_struct_sizes_match_header():

@@ -80,3 +80,34 @@ def test_python_layer_maps_statuses(env):
         cost_estimate(InstructionMix({OpClass.FP32: 3}, 0), 10.0)
     with pytest.raises(ValueError):
         cost_estimate(InstructionMix({OpClass.FP32: 3}, 0), 3.5, scale=0.0)
+
+
+def test_score_space_flags_checked(env):
+    torch, L, lib, plan, rec = env
+    out = torch.empty((plan.n_seg, plan.k), dtype=torch.int64, device="cuda")
+
+    def call(flags):
+        return lib.occx_score_space(
+            plan._ctx, L.ptr(plan.h_archs), plan.n_arch, L.ptr(plan.d_desc), plan.n_seg,
+            L.ptr(plan.d_pool), plan.n_pool, 0, plan.total, 0, 0, flags, L.ptr(plan.d_vtab),
+            plan.n_var, plan.n_seg, plan.k, L.ptr(plan.d_ws), plan.ws_bytes, L.ptr(out),
+            L.stream_ptr())
+    assert call(0) == 0 and call(L.SCORE_EVERY_KEY) == 0
+    assert call(0x2) == 1                                 # unknown flag bit: ValueError
+
+
+@pytest.mark.parametrize("options", [1, 2, 3])
+def test_ctx_options_same_topk(env, options):
+    """The LDG-fed K2 (two 512-thread CTAs per SM, doubled workspace) and the
+    one-slice TMA ring give the default's top-k on config 2 (golden)."""
+    from helpers import load_golden
+    from paper_1701_08547_b200 import ScorePlan, workloads
+    torch, L, lib, _, _ = env
+    h = L.ctx(options=options)
+    assert lib.occx_ctx_options(h) == options
+    cfg = workloads.config2()
+    plan = ScorePlan(cfg.kernels, cfg.archs, k=cfg.k, options=options)
+    if options & L.CTX_K2_FEED_LDG:
+        assert plan.grid_lists == 2 * lib.occx_ctx_sm_count(h)
+    got = plan.score(plan.generate(), plan.total).cpu().numpy().view(np.uint64)
+    assert got.reshape(plan.n_seg, plan.k).tolist() == load_golden("topk_config2.json")["corrected"]

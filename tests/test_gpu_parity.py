@@ -139,6 +139,45 @@ def test_k1_random_mixes_golden(P, golden):
             assert fb.intensity[m].hex() == v["intensity"]
 
 
+def test_k1_naive_sum_mode_vs_oracle(P, golden):
+    """OCCX_SUM_NAIVE (CPython <= 3.11 sum(), the reference's recorded run on
+    3.10.12): K1 with sum_mode=1 on the 3000 random mixes and the 40 workload
+    variants equals pyref under sum_semantics("naive") as hex -- cost,
+    cycles, coefficients, shares -- and differs from the compensated mode on
+    some sm35 mixes, so the branch is exercised (mix.py:278, :330, :349)."""
+    from oracle import pyref
+    from paper_1701_08547_b200.batch import feature_score
+    g = golden("mix.json")
+    items = [(dict(v["counts"]), v["reg_operands"], v["cc"], float.fromhex(v["scale"]))
+             for v in g["random"]]
+    items += [(dict(v["counts"]), v["reg_operands"], cc, 1.0)
+              for v in g["variants"] for cc in (2.0, 3.5, 5.2, 6.0)]
+    by_key = {}
+    for i, (_, _, cc, scale) in enumerate(items):
+        by_key.setdefault((cc, scale), []).append(i)
+    differ = checked = 0
+    for (cc, scale), idx in by_key.items():
+        mixes = [_mix(P, items[i][0].items(), items[i][1]) for i in idx]
+        naive = feature_score(mixes, [cc], scale=scale, sum_mode=1)
+        comp = feature_score(mixes, [cc], scale=scale, sum_mode=0)
+        for m, i in enumerate(idx):
+            counts, regs = items[i][0], items[i][1]
+            got = naive.one(m, 0)
+            with pyref.sum_semantics("naive"):
+                cost = pyref.cost_estimate(counts, regs, cc, scale)
+                cyc = pyref.category_cycles(counts, regs, cc)
+                shares = pyref.pipeline_utilization(counts, regs, cc)
+                coef = pyref._flops_coefficient(counts, pyref.column(cc))
+            assert got.cost.hex() == cost.hex(), (cc, counts)
+            assert [x.hex() for x in got.cycles.values()] == [x.hex() for x in cyc.values()]
+            assert [x.hex() for x in got.shares.values()] == [x.hex() for x in shares.values()]
+            assert list(got.coefficients.values())[0].hex() == coef.hex()
+            differ += got.cost != comp.one(m, 0).cost
+            checked += 1
+    assert checked == len(items)
+    assert differ > 0, "sum_mode=1 never differed from the compensated mode"
+
+
 # ---------------------------------------------------------------------------
 # K0: aggregate
 # ---------------------------------------------------------------------------

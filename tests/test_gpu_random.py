@@ -76,12 +76,8 @@ def test_random_spaces_k2_k2i_vs_oracle(seed):
         rec = plan.generate()
         got = plan.score(rec, plan.total).cpu().numpy().view(np.uint64)
         assert np.array_equal(got, want), (seed, mode)
-        for prune in ("1", "0"):           # block-bound pruning on (default) and off
-            os.environ["OCCX_K2I_PRUNE"] = prune
-            try:
-                got_i = plan.score_implicit().cpu().numpy().view(np.uint64)
-            finally:
-                os.environ.pop("OCCX_K2I_PRUNE", None)
+        for prune in (True, False):        # block-bound pruning on (default) and off
+            got_i = plan.score_implicit(prune=prune).cpu().numpy().view(np.uint64)
             assert np.array_equal(got_i, want), (seed, mode, "implicit", prune)
 
 
@@ -260,11 +256,7 @@ def test_random_big_blocks_k2i_vs_oracle(seed):
         plan = P.ScorePlan(cfg.kernels, cfg.archs, mode, k=cfg.k)
         got_i = plan.score_implicit().cpu().numpy().view(np.uint64)
         assert np.array_equal(got_i, want), (seed, mode, "implicit")
-        os.environ["OCCX_K2I_PRUNE"] = "0"
-        try:
-            got_f = plan.score_implicit().cpu().numpy().view(np.uint64)
-        finally:
-            os.environ.pop("OCCX_K2I_PRUNE", None)
+        got_f = plan.score_implicit(prune=False).cpu().numpy().view(np.uint64)
         assert np.array_equal(got_f, want), (seed, mode, "implicit, no pruning")
         rec = plan.generate()
         for b, n in ((0, plan.total), (rng.randrange(plan.total), None)):

@@ -173,3 +173,30 @@ def test_pyref_topk_config1(golden):
     top = [pyref.key_index(k) for k in g["corrected"][0]]
     assert [32 * (i + 1) for i in top] == [128, 256, 512, 1024, 224, 288, 672, 992, 160,
                                            192, 320, 384, 480, 640, 960, 928]
+
+
+def test_pyref_naive_sum_semantics(golden):
+    """CPython <= 3.11 sum() (the reference's recorded run, Python 3.10.12,
+    /root/reference/pkg/test_output.txt:2): pyref under sum_semantics("naive")
+    equals an independent left-to-right float64 accumulation (np.cumsum)
+    of the same terms, and differs from this interpreter's compensated
+    sum() on some sm35 mixes (so the mode is observable)."""
+    import sys
+    g = golden("mix.json")
+    differ = 0
+    for v in g["random"]:
+        counts = dict(v["counts"])
+        regs, cc, scale = v["reg_operands"], v["cc"], float.fromhex(v["scale"])
+        col = pyref.column(cc)
+        fl = [n * pyref.cpi(c, col) for c, n in counts.items() if pyref.CATEGORY.get(c) == "FLOPS"]
+        nfl = pyref.flops(counts)
+        coef = np.cumsum(fl)[-1] / nfl if nfl else pyref.cpi("FPIns32", col)
+        terms = [coef * nfl, pyref.cpi("LdStIns", col) * pyref.mem(counts),
+                 pyref.cpi("CtrlIns", col) * pyref.ctrl(counts), pyref.cpi("Regs", col) * regs]
+        want = scale * float(np.cumsum(terms)[-1])
+        with pyref.sum_semantics("naive"):
+            got = pyref.cost_estimate(counts, regs, cc, scale)
+        assert got.hex() == want.hex()
+        differ += got != pyref.cost_estimate(counts, regs, cc, scale)
+    if sys.version_info >= (3, 12):
+        assert differ > 0, "naive and compensated sum() never differ on the golden mixes"

@@ -10,9 +10,9 @@ from helpers import load_golden
 from paper_1701_08547_b200 import sass, workloads
 
 
-def _summary(text):
+def _summary(text, chunk_bytes=0):
     try:
-        r = sass.tokenize(text)
+        r = sass.tokenize(text, chunk_bytes)
     except Exception as exc:
         from paper_1701_08547_b200.errors import StaticAnalysisError
         return ["err", type(exc).__name__, getattr(exc, "line", None), str(exc)]
@@ -68,7 +68,7 @@ def test_corpus_aggregate_golden_via_tokenizer():
         assert int(regs[k]) == reg
 
 
-def test_chunked_parse_equals_single_chunk(monkeypatch):
+def test_chunked_parse_equals_single_chunk():
     """Force tiny chunks (many threads): identical results and errors."""
     g = load_golden("sass_fuzz.json")
     texts = [c["text"] for c in g["cases"][:600]]
@@ -77,6 +77,5 @@ def test_chunked_parse_equals_single_chunk(monkeypatch):
     texts.append(workloads.corpus_text(c))
     texts.append(big)
     single = [_summary(t) for t in texts]
-    monkeypatch.setenv("OCCX_SASS_CHUNK_BYTES", "97")
-    multi = [_summary(t) for t in texts]
+    multi = [_summary(t, 97) for t in texts]
     assert multi == single
