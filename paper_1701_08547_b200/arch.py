@@ -213,16 +213,22 @@ def cost_key(spec: ArchSpec) -> int:
 def device_limits_ok(spec: ArchSpec) -> str | None:
     """None when the packed form can represent ``spec`` exactly, else why not.
 
-    Limits of the device tables (hold for every shipped NVIDIA GPU):
-    power-of-two warp size, <= 64 warps per block, <= 1023 registers per
-    thread, <= 255 blocks and <= 127 warps per SM (u8 / 7-bit key
-    fields), shared memory below 2**24 bytes.
+    Limits of the device tables (hold for every shipped NVIDIA GPU); the
+    same set ``occx_check_archs`` (csrc/occx_score.cu) enforces, so an arch
+    either fails here with its field named or is accepted by every kernel:
+    power-of-two warp size, <= 64 warps per block, fewer than 2048 threads
+    per block (the static / rule membership masks cover T/32 < 64), <= 1023
+    registers per thread, <= 255 blocks and <= 127 warps per SM (u8 / 7-bit
+    key fields), register file and allocation granularity below 2**20,
+    shared memory below 2**24 bytes.
     """
     ws = spec.warp_size
-    if ws & (ws - 1):
+    if ws <= 0 or ws & (ws - 1):
         return "warp_size must be a power of two"
     if spec.max_threads_per_block // ws > 64:
         return "more than 64 warps per block"
+    if spec.max_threads_per_block >= 2048:
+        return "max_threads_per_block at or above 2048 (membership masks cover T < 2048)"
     if spec.max_regs_per_thread > 1023:
         return "max_regs_per_thread above 1023"
     if spec.max_blocks_per_mp > 255:
@@ -231,8 +237,10 @@ def device_limits_ok(spec: ArchSpec) -> str | None:
         return "max_warps_per_mp above 127"
     if spec.shared_mem_per_block >= 1 << 24:
         return "shared_mem_per_block at or above 2**24"
-    if spec.register_file_size >= 1 << 24:
-        return "register_file_size at or above 2**24"
+    if spec.register_file_size >= 1 << 20:
+        return "register_file_size at or above 2**20"
+    if spec.register_alloc_granularity >= 1 << 20:
+        return "register_alloc_granularity at or above 2**20"
     return None
 
 

@@ -37,22 +37,29 @@ def _stale(obj: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False) -> str:
-    """Compile the stale sources (in parallel) and link liboccx.so."""
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, timing: bool = False) -> str:
+    """Compile the stale sources (in parallel) and link liboccx.so.
+    ``timing``: the instrumented K2 build (-DOCCX_K2_TIMING: per-CTA
+    globaltimer spans and slow-path counters, scripts/k2_profile.py) into
+    _objs_timing/liboccx_timing.so -- experiments only, never loaded by
+    the package unless OCCX_LIB names it."""
+    build_dir = BUILD + ("_timing" if timing else "")
+    out = os.path.join(build_dir, "liboccx_timing.so") if timing else OUT
+    defs = ["-DOCCX_K2_TIMING"] if timing else []
+    os.makedirs(build_dir, exist_ok=True)
     header_deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)
                    if f.endswith((".cuh", ".h"))]
     header_deps += [os.path.join(os.path.dirname(HERE), "include", "occx.h"), __file__]
     objs, jobs = [], []
     for src, extra in SOURCES.items():
         path = os.path.join(CSRC, src)
-        obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+        obj = os.path.join(build_dir, src.replace(".cu", ".o"))
         objs.append(obj)
         if _stale(obj, [path] + header_deps):
-            jobs.append((src, [NVCC, *ARCH, *COMMON, *extra, "-c", path, "-o", obj]))
+            jobs.append((src, [NVCC, *ARCH, *COMMON, *defs, *extra, "-c", path, "-o", obj]))
     for src, extra in CXX_SOURCES.items():
         path = os.path.join(CSRC, src)
-        obj = os.path.join(BUILD, src.replace(".cpp", ".o"))
+        obj = os.path.join(build_dir, src.replace(".cpp", ".o"))
         objs.append(obj)
         if _stale(obj, [path] + header_deps):
             jobs.append((src, [CXX, "-O3", "-std=c++17", "-fPIC", "-Wall", "-c", path,
@@ -61,21 +68,21 @@ def build(verbose: bool = False) -> str:
                                     text=True)) for src, cmd in jobs]
     failed = []
     for src, pr in procs:
-        out, _ = pr.communicate()
+        log, _ = pr.communicate()
         if verbose or pr.returncode:
-            sys.stderr.write(out)
+            sys.stderr.write(log)
         if pr.returncode:
             failed.append(src)
     if failed:
         raise RuntimeError(f"compile failed on {', '.join(failed)}")
-    if _stale(OUT, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", OUT, *objs]
+    if _stale(out, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", out, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError("link of liboccx.so failed")
-    return OUT
+            raise RuntimeError(f"link of {os.path.basename(out)} failed")
+    return out
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    print(build(verbose="-v" in sys.argv, timing="--timing" in sys.argv))

@@ -985,11 +985,17 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
 }
 
 #ifdef OCCX_K2_TIMING
-// experiment-only (scratch/k2_timing.sh): per-CTA {start, end, smid, tiles}
-__device__ uint64_t g_k2_timing[4 * 1024];
+// experiment-only (scripts/k2_profile.py): per CTA {entry, after setup,
+// consumers done, end, smid, tiles, 0, 0} (globaltimer ns)
+__device__ uint64_t g_k2_timing[8 * 1024];
+__device__ __forceinline__ uint64_t k2_gt() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 }  // namespace
 extern "C" int occx_debug_k2_timing(uint64_t* out, int n) {
-  return cudaMemcpyFromSymbol(out, g_k2_timing, (size_t)n * 4 * 8) == cudaSuccess ? 0 : 6;
+  return cudaMemcpyFromSymbol(out, g_k2_timing, (size_t)n * 8 * 8) == cudaSuccess ? 0 : 6;
 }
 extern "C" int occx_debug_k2_counts(uint64_t* out, int n, int reset) {
   if (cudaMemcpyFromSymbol(out, g_k2_cnt, (size_t)n * 8 * 8) != cudaSuccess) return 6;
@@ -1021,6 +1027,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
   const uint32_t n_tiles = begin < end ? (uint32_t)((end - begin + kTmaTile - 1) / kTmaTile) : 0u;
   const uint32_t first = n_tiles < (uint32_t)kTmaStages ? n_tiles : (uint32_t)kTmaStages;
   uint64_t policy = 0;
+#ifdef OCCX_K2_TIMING
+  if (threadIdx.x == 0) g_k2_timing[blockIdx.x * 8 + 0] = k2_gt();
+#endif
   if (threadIdx.x == 0) {
     for (int i = 0; i < kTmaStages; ++i) {
       mbar_init(&full[i], 1);
@@ -1042,12 +1051,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
   __syncthreads();
 #ifdef OCCX_K2_TIMING
   if (threadIdx.x == 0) {
-    uint64_t t0; uint32_t sm;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    uint32_t sm;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-    g_k2_timing[blockIdx.x * 4 + 0] = t0;
-    g_k2_timing[blockIdx.x * 4 + 2] = sm;
-    g_k2_timing[blockIdx.x * 4 + 3] = n_tiles;
+    g_k2_timing[blockIdx.x * 8 + 1] = k2_gt();
+    g_k2_timing[blockIdx.x * 8 + 4] = sm;
+    g_k2_timing[blockIdx.x * 8 + 5] = n_tiles;
   }
 #endif
   if (warp == 0) {
@@ -1113,16 +1121,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
     k2_stage(wl, lane, p.k, stage, warp - 1, kTmaConsumerWarps);
   }
   __syncthreads();
+#ifdef OCCX_K2_TIMING
+  if (threadIdx.x == 0) g_k2_timing[blockIdx.x * 8 + 2] = k2_gt();
+#endif
   if (warp == 1) k2_merge_staged(stage, 2 * kTmaConsumerWarps, p.k, s.thr, s.list, s.lock);
   __syncthreads();
   k2_flush(p, s);
 #ifdef OCCX_K2_TIMING
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint64_t t1;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-    g_k2_timing[blockIdx.x * 4 + 1] = t1;
-  }
+  if (threadIdx.x == 0) g_k2_timing[blockIdx.x * 8 + 3] = k2_gt();
 #endif
 }
 
@@ -1385,7 +1392,9 @@ extern "C" int occx_check_archs(const occx_arch_t* h, int n, int* bad) {
     const occx_arch_t& a = h[i];
     bool ok = a.warp_size > 0 && (a.warp_size & (a.warp_size - 1)) == 0 &&
               a.max_threads_per_block > 0 && a.max_threads_per_block % a.warp_size == 0 &&
-              a.max_threads_per_block / a.warp_size <= kMaxWpb && a.max_blocks_per_mp > 0 &&
+              a.max_threads_per_block / a.warp_size <= kMaxWpb &&
+              a.max_threads_per_block < 2048 &&          // membership masks: T/32 < 64
+              a.max_blocks_per_mp > 0 &&
               a.max_blocks_per_mp <= 255 && a.max_warps_per_mp > 0 && a.max_warps_per_mp <= 127 &&
               a.register_file_size > 0 && a.register_file_size < (1 << 20) &&
               a.register_alloc_granularity > 0 && a.register_alloc_granularity < (1 << 20) &&

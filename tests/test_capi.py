@@ -87,3 +87,42 @@ def test_null_arguments_rejected(lib):
     assert lib.occx_score_topk(None, None, 0, None, 0, 0, 0, None, 0, 0, 0, None, 0,
                                None, None) == 1
     assert lib.occx_topk_merge(None, None, 0, 0, 0, None, None) == 1
+
+
+def _spec(**kw):
+    from dataclasses import replace
+    base = workloads.all_archs()[4]            # sm_100 INI table
+    return replace(base, **kw)
+
+
+@pytest.mark.parametrize("field,value", [
+    ("max_threads_per_block", 2048),            # T = 2048 outside the 64-bit masks
+    ("register_file_size", 1 << 20),
+    ("register_alloc_granularity", 1 << 20),
+    ("max_blocks_per_mp", 256),
+    ("shared_mem_per_block", 1 << 24),
+])
+def test_host_and_device_limits_agree(lib, field, value):
+    """arch.device_limits_ok and occx_check_archs enforce one set of limits:
+    an arch the device tables cannot hold fails in pack_archs with
+    ArchSpecError naming it, and the C check rejects the same row."""
+    from paper_1701_08547_b200.arch import device_limits_ok
+    from paper_1701_08547_b200.errors import ArchSpecError
+    kw = {field: value}
+    if field == "max_threads_per_block":
+        kw["max_warps_per_mp"] = 64
+    try:
+        s = _spec(**kw)
+    except Exception:                            # the reference's own invariants reject it
+        pytest.skip("not a valid ArchSpec")
+    assert device_limits_ok(s)
+    with pytest.raises(ArchSpecError):
+        pack_archs([s])
+    ok = _spec()
+    row = pack_archs([ok])
+    for f, v in kw.items():
+        row[0][f] = v
+    bad = ctypes.c_int(0)
+    assert lib.occx_check_archs(row.ctypes.data, 1, ctypes.byref(bad)) == 8 and bad.value == 0
+    assert device_limits_ok(ok) is None
+    assert lib.occx_check_archs(pack_archs([ok]).ctypes.data, 1, ctypes.byref(bad)) == 0
