@@ -133,19 +133,23 @@ typedef struct occx_mixsum_t {
 
 /* Per (mix, column) Eq. 6 features.  Index order FLOPS, MEM, CTRL, REG.
  * per_class[r] by CPI row (14 classes, Regs at 14); NaN when the reference
- * omits the row (mix.py:309-318).  status OK / UNSUPPORTED_ARCH / KEY.    */
+ * omits the row (mix.py:309-318).  status: OK / UNSUPPORTED_ARCH / KEY for
+ * the lookups cost, coef, cycles and shares make (mix.py:268-306; cost and
+ * cycles/shares are NaN on KEY); pc_status: the same for the lookups
+ * per_class_cycles makes (mix.py:309-318).  A partial throughput table can
+ * fail one set and not the other, exactly as the reference raises.       */
 typedef struct occx_feat_t {
   double cost;            /* cost_estimate(mix, cc, scale)  mix.py:321-330 */
   double coef[4];         /* category_coefficients          mix.py:284-293 */
   double cycles[4];       /* category_cycles                mix.py:296-306 */
   double shares[4];       /* pipeline_utilization           mix.py:340-352 */
   double per_class[16];   /* per_class_cycles               mix.py:309-318 */
-  int32_t status, reserved;
+  int32_t status, pc_status;
 } occx_feat_t;
 
 /* One (variant, arch) row of the scorer's feature table.  32 B.
- * member: 128-bit interleaved membership, for b = t/32 (t % 32 == 0,
- * b < 64): bit 2b = t survives static_prune, bit 2b+1 = t survives
+ * member: 128-bit interleaved membership, for b = t/32 - 1 (t % 32 == 0,
+ * 32 <= t <= 2048): bit 2b = t survives static_prune, bit 2b+1 = t survives
  * rule_prune (tuning.py:94-127) for this segment, the rule half already
  * chosen by the variant's intensity.  rank_bits = 2^20-1 - dense cost rank
  * among the kernel's variants on this arch, 0 when the arch has no cost

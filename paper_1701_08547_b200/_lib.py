@@ -36,7 +36,7 @@ MIXSUM = np.dtype([("intensity", "<f8"), ("flops", "<u8"), ("mem", "<u8"),
                    ("ctrl", "<u8"), ("unclassified", "<u8"), ("total", "<u8")])
 FEAT = np.dtype([("cost", "<f8"), ("coef", "<f8", 4), ("cycles", "<f8", 4),
                  ("shares", "<f8", 4), ("per_class", "<f8", 16),
-                 ("status", "<i4"), ("reserved", "<i4")])
+                 ("status", "<i4"), ("pc_status", "<i4")])
 VENT = np.dtype([("member", "<u4", 4), ("seg", "<u4"), ("key_hi", "<u4"),
                  ("rank_bits", "<u4"), ("reserved", "<u4")])
 SEGDESC = np.dtype([("start", "<u8"), ("size", "<u8"), ("arch", "<u4"),

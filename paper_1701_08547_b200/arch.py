@@ -216,8 +216,9 @@ def device_limits_ok(spec: ArchSpec) -> str | None:
     Limits of the device tables (hold for every shipped NVIDIA GPU); the
     same set ``occx_check_archs`` (csrc/occx_score.cu) enforces, so an arch
     either fails here with its field named or is accepted by every kernel:
-    power-of-two warp size, <= 64 warps per block, fewer than 2048 threads
-    per block (the static / rule membership masks cover T/32 < 64), <= 1023
+    power-of-two warp size, <= 64 warps per block, at most 2048 threads
+    per block (the static / rule membership masks hold bit T/32 - 1 < 64;
+    every warp-size-32 arch fits), <= 1023
     registers per thread, <= 255 blocks and <= 127 warps per SM (u8 / 7-bit
     key fields), register file and allocation granularity below 2**20,
     shared memory below 2**24 bytes.
@@ -227,8 +228,8 @@ def device_limits_ok(spec: ArchSpec) -> str | None:
         return "warp_size must be a power of two"
     if spec.max_threads_per_block // ws > 64:
         return "more than 64 warps per block"
-    if spec.max_threads_per_block >= 2048:
-        return "max_threads_per_block at or above 2048 (membership masks cover T < 2048)"
+    if spec.max_threads_per_block > 2048:
+        return "max_threads_per_block above 2048 (membership masks cover T <= 2048)"
     if spec.max_regs_per_thread > 1023:
         return "max_regs_per_thread above 1023"
     if spec.max_blocks_per_mp > 255:

@@ -356,7 +356,16 @@ class Features:
     coefficients: dict
     cycles: dict
     shares: dict
-    per_class: dict
+    per_class_map: dict | None      # None: a class in use has no CPI entry
+
+    @property
+    def per_class(self) -> dict:
+        """per_class_cycles (ref mix.py:309-318): raises KeyError like the
+        reference when the table lacks a row the mix uses, independently of
+        whether the cost lookups succeeded."""
+        if self.per_class_map is None:
+            raise KeyError("throughput table has no entry for a class in use")
+        return self.per_class_map
 
 
 @dataclass
@@ -371,29 +380,32 @@ class FeatureBatch:
     def intensity(self) -> list[float]:
         return [float(x) for x in self.sums["intensity"]]
 
-    def one(self, m: int, j: int) -> Features:
+    def one(self, m: int, j: int, need_cost: bool = True) -> Features:
         f = self.feat[m * self.n_col + j]
         st = int(f["status"])
         cc = self.ccs[j]
         if st == 3:
             from .mix import sm_key
             sm_key(cc)                      # raises UnsupportedArchitectureError
-        if st == 9:
+        if st == 9 and need_cost:
             raise KeyError("throughput table has no entry for a class in use")
-        _lib.check(st, "occx_feature_score")
+        if st not in (0, 9):
+            _lib.check(st, "occx_feature_score")
         mix = self.mixes[m]
-        per_class = {}
-        for cls in mix.counts:
-            if cls is not OpClass.UNCLASSIFIED and mix.counts[cls]:
-                per_class[cls] = float(f["per_class"][CPI_ROW[cls]])
-        if mix.reg_operands:
-            per_class[OpClass.REGS] = float(f["per_class"][CPI_ROW[OpClass.REGS]])
+        per_class = None
+        if int(f["pc_status"]) == 0:
+            per_class = {}
+            for cls in mix.counts:
+                if cls is not OpClass.UNCLASSIFIED and mix.counts[cls]:
+                    per_class[cls] = float(f["per_class"][CPI_ROW[cls]])
+            if mix.reg_operands:
+                per_class[OpClass.REGS] = float(f["per_class"][CPI_ROW[OpClass.REGS]])
         return Features(
             cost=float(f["cost"]),
             coefficients={c: float(f["coef"][i]) for i, c in enumerate(_CATS)},
             cycles={c: float(f["cycles"][i]) for i, c in enumerate(_CATS)},
             shares={c: float(f["shares"][i]) for i, c in enumerate(_CATS)},
-            per_class=per_class)
+            per_class_map=per_class)
 
 
 def feature_records(d_mix, n_mix: int, cols: Sequence[int], cpi: np.ndarray, scale: float,

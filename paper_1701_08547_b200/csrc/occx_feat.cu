@@ -77,17 +77,22 @@ __global__ void feature_kernel(const __grid_constant__ FeatParams p) {
   if (p.n_col == 0) return;
   occx_feat_t f;
   for (int i = 0; i < 16; ++i) f.per_class[i] = NAN;
-  f.reserved = 0;
+  f.pc_status = 0;
   const int key = p.cols[j];
   if (key < 0 || key > 3) {                       // sm_key raises, mix.py:99-106
-    f.status = OCCX_ERR_UNSUPPORTED_ARCH;
+    f.status = f.pc_status = OCCX_ERR_UNSUPPORTED_ARCH;
     f.cost = NAN;
     for (int i = 0; i < 4; ++i) f.coef[i] = f.cycles[i] = f.shares[i] = NAN;
     p.feat[t] = f;
     return;
   }
   const double* cp = p.cpi[key];
-  bool missing = false;
+  // Two lookup sets, as in the reference: cost / coefficients / cycles /
+  // shares need the FLOPS classes present (or FP32) plus LdSt, Ctrl, Regs
+  // (mix.py:268-306); per_class_cycles needs every class with n != 0 and
+  // Regs when reg_operands != 0 (mix.py:309-318).  A partial table can fail
+  // one and not the other.
+  bool missing = false, pc_missing = false;
   // _flops_coefficient, mix.py:268-281
   double coef_f;
   if (flops == 0) {
@@ -131,11 +136,19 @@ __global__ void feature_kernel(const __grid_constant__ FeatParams p) {
   // per_class_cycles, mix.py:309-318 (n != 0 only; Unclassified excluded)
   for (int c = 0; c < 14; ++c)
     if (mx.first_key[c] != kAbsent && mx.counts[c] != 0) {
-      missing |= isnan(cp[c]);
+      pc_missing |= isnan(cp[c]);
       f.per_class[c] = __dmul_rn((double)mx.counts[c], cp[c]);
     }
-  if (mx.reg_operands != 0) f.per_class[kRegsRow] = __dmul_rn((double)mx.reg_operands, cp[kRegsRow]);
+  if (mx.reg_operands != 0) {
+    pc_missing |= isnan(cp[kRegsRow]);
+    f.per_class[kRegsRow] = __dmul_rn((double)mx.reg_operands, cp[kRegsRow]);
+  }
+  if (missing) {                // cost_estimate raises: no cost enters any rank
+    f.cost = NAN;
+    for (int i = 0; i < 4; ++i) f.cycles[i] = f.shares[i] = NAN;
+  }
   f.status = missing ? OCCX_ERR_KEY : OCCX_OK;
+  f.pc_status = pc_missing ? OCCX_ERR_KEY : OCCX_OK;
   p.feat[t] = f;
 }
 

@@ -123,7 +123,7 @@ __device__ __forceinline__ void k2_fill(const K2Ctx& c, const uint4 r, K2Cache& 
   const uint32_t v = r.x;
   const uint32_t vcl = min(v, c.n_var - 1);
   const occx_vent_t* e = c.vt + (vcl * c.n_arch + ac);
-  const uint32_t tb = T >> 5;
+  const uint32_t tb = (T >> 5) - 1u;   // mask bit of T = 32 (b + 1): T in [32, 2048]
   uint2 sh;            // {seg, key_hi}
   uint32_t word;
   if (VT_SMEM) {       // explicit address spaces: LDS for the smem copy, LDG.NC otherwise
@@ -135,7 +135,7 @@ __device__ __forceinline__ void k2_fill(const K2Ctx& c, const uint4 r, K2Cache& 
     word = __ldg(&e->member[(tb >> 4) & 3u]);
   }
   uint32_t bits = (word >> ((tb & 15u) << 1)) & 3u;
-  bits = (T & 0xF81Fu) ? 0u : bits;                                  // T % 32 == 0, T < 2048
+  bits = ((T & 31u) | (tb >> 6)) ? 0u : bits;                       // T % 32 == 0, 32 <= T <= 2048
   k.x = r.x;
   k.z = r.z;
   k.w = r.w;

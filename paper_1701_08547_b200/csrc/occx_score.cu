@@ -344,6 +344,7 @@ __device__ inline void k2_merge_staged(const uint64_t* stage, uint32_t n_slots, 
     mine = list_merge_sorted(mine, key, lane, k);
     if (lane < (int)k) s_list[seg * k + lane] = mine;
     const uint64_t thr = warp_list_min(mine, (int)k);
+    __syncwarp();                      // every lane's s_thr[seg] read above is done
     if (lane == 0) s_thr[seg] = thr;
     __syncwarp();
   }
@@ -1393,7 +1394,7 @@ extern "C" int occx_check_archs(const occx_arch_t* h, int n, int* bad) {
     bool ok = a.warp_size > 0 && (a.warp_size & (a.warp_size - 1)) == 0 &&
               a.max_threads_per_block > 0 && a.max_threads_per_block % a.warp_size == 0 &&
               a.max_threads_per_block / a.warp_size <= kMaxWpb &&
-              a.max_threads_per_block < 2048 &&          // membership masks: T/32 < 64
+              a.max_threads_per_block <= 2048 &&         // membership masks: bit T/32 - 1 < 64
               a.max_blocks_per_mp > 0 &&
               a.max_blocks_per_mp <= 255 && a.max_warps_per_mp > 0 && a.max_warps_per_mp <= 127 &&
               a.register_file_size > 0 && a.register_file_size < (1 << 20) &&

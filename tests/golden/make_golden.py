@@ -11,6 +11,8 @@ with sys.version (CPython's float sum() changed in 3.12):
                          (T 1..1100, R 0..300), limit_by_smem S 0..Smax+64
   occupancy_random.npz   200k random occupancy() calls, every field
   suggest.json           suggest() over archs x regs x smem x modes
+  partial_table.json     cost / cycles / shares / per_class outcomes (hex or
+                         KeyError) under partial throughput tables
   mix.json               ATAX fixture aggregate, workload variant features,
                          3000 random mixes (cost/intensity/shares as hex)
   corpus.json            aggregate() of the reference parser over the first
@@ -190,6 +192,52 @@ def mix_golden():
                      "intensity": R.intensity(rm).hex(), "features": _features(rm, cc)})
     with open(os.path.join(HERE, "mix.json"), "w") as fh:
         json.dump({"meta": META, "atax": atax, "variants": variants, "random": rand}, fh)
+
+
+def _outcome_of(f):
+    try:
+        v = f()
+    except KeyError:
+        return "KeyError"
+    if isinstance(v, dict):
+        return {(c.value if hasattr(c, "value") else c): x.hex() for c, x in v.items()}
+    return v.hex()
+
+
+def partial_table_golden(n=600):
+    """Partial throughput tables: each table drops a random set of
+    (class, key) entries; record what cost_estimate / category_cycles /
+    pipeline_utilization / per_class_cycles return or raise (KeyError)."""
+    rng = random.Random(0x9A57)
+    classes = [c for c in R.OpClass if c is not R.OpClass.UNCLASSIFIED]
+    full = dict(Rmix.DEFAULT_THROUGHPUT.ipc)
+    rows = []
+    for i in range(n):
+        drop = set()
+        for _ in range(rng.choice((1, 1, 2, 3))):
+            drop.add((rng.choice(classes), rng.choice(Rmix.SM_KEYS)))
+        ipc = {k: v for k, v in full.items() if k not in drop}
+        table = Rmix.ThroughputTable(ipc=ipc)
+        k = rng.randrange(0, 6)
+        picked = rng.sample([c for c in classes if c is not R.OpClass.REGS]
+                            + [R.OpClass.UNCLASSIFIED], k)
+        if rng.random() < 0.5 and drop:        # make a dropped class likely in use
+            c0 = next(iter(drop))[0]
+            if c0 is not R.OpClass.REGS and c0 not in picked:
+                picked.append(c0)
+        counts = [[c.value, rng.choice((0, 1, 5, 40))] for c in picked]
+        regs = rng.choice((0, 0, 3, 77))
+        mx = R.InstructionMix({R.OpClass(c): m for c, m in counts}, regs)
+        cc = rng.choice((2.0, 3.5, 5.2, 6.0))
+        rows.append({
+            "drop": [[c.value, key] for c, key in sorted(drop, key=lambda t: (t[0].value, t[1]))],
+            "counts": counts, "reg_operands": regs, "cc": cc,
+            "cost": _outcome_of(lambda: R.cost_estimate(mx, cc, 1.0, table)),
+            "cycles": _outcome_of(lambda: Rmix.category_cycles(mx, cc, table)),
+            "shares": _outcome_of(lambda: R.pipeline_utilization(mx, cc, table)),
+            "per_class": _outcome_of(lambda: Rmix.per_class_cycles(mx, cc, table))})
+    with open(os.path.join(HERE, "partial_table.json"), "w") as fh:
+        json.dump({"meta": META, "rows": rows}, fh)
 
 
 def corpus_golden(n_kernels=2000):
@@ -651,7 +699,7 @@ if __name__ == "__main__":
     for s in steps:
         t0 = time.time()
         {"tables": occupancy_tables, "random": occupancy_random, "suggest": suggest_golden,
-         "mix": mix_golden, "corpus": corpus_golden, "sass": sass_golden,
+         "mix": mix_golden, "partial": partial_table_golden, "corpus": corpus_golden, "sass": sass_golden,
          "report": report_golden, "specs": specs_golden}.get(
             s, lambda: topk_golden(s))()
         print(f"{s}: {time.time() - t0:.1f}s", flush=True)

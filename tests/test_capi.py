@@ -96,7 +96,7 @@ def _spec(**kw):
 
 
 @pytest.mark.parametrize("field,value", [
-    ("max_threads_per_block", 2048),            # T = 2048 outside the 64-bit masks
+    ("max_threads_per_block", 4096),            # T = 4096 (warp size 64) outside the 64-bit masks
     ("register_file_size", 1 << 20),
     ("register_alloc_granularity", 1 << 20),
     ("max_blocks_per_mp", 256),
@@ -110,7 +110,7 @@ def test_host_and_device_limits_agree(lib, field, value):
     from paper_1701_08547_b200.errors import ArchSpecError
     kw = {field: value}
     if field == "max_threads_per_block":
-        kw["max_warps_per_mp"] = 64
+        kw.update(warp_size=64, max_warps_per_mp=64, max_threads_per_mp=64 * 64)
     try:
         s = _spec(**kw)
     except Exception:                            # the reference's own invariants reject it
@@ -121,8 +121,19 @@ def test_host_and_device_limits_agree(lib, field, value):
     ok = _spec()
     row = pack_archs([ok])
     for f, v in kw.items():
-        row[0][f] = v
+        if f in row.dtype.names:
+            row[0][f] = v
     bad = ctypes.c_int(0)
     assert lib.occx_check_archs(row.ctypes.data, 1, ctypes.byref(bad)) == 8 and bad.value == 0
     assert device_limits_ok(ok) is None
     assert lib.occx_check_archs(pack_archs([ok]).ctypes.data, 1, ctypes.byref(bad)) == 0
+
+
+def test_t2048_arch_accepted(lib):
+    """64 warps of 32 threads (max_threads_per_block 2048) is inside the
+    device tables: T = 2048 is mask bit 63."""
+    from paper_1701_08547_b200.arch import device_limits_ok
+    s = _spec(max_threads_per_block=2048, max_threads_per_mp=2048, max_warps_per_mp=64)
+    assert device_limits_ok(s) is None
+    bad = ctypes.c_int(0)
+    assert lib.occx_check_archs(pack_archs([s]).ctypes.data, 1, ctypes.byref(bad)) == 0

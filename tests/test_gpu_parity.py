@@ -122,6 +122,43 @@ def test_k1_features_golden(P, golden):
             assert {c.value: x.hex() for c, x in got.per_class.items()} == f["per_class"]
 
 
+def test_k1_partial_throughput_table_golden(P, golden):
+    """A custom ThroughputTable missing entries: cost / category_cycles /
+    pipeline_utilization raise KeyError exactly when the reference's cost
+    lookups do (mix.py:268-306), per_class_cycles exactly when its own
+    lookups do (mix.py:309-318) -- the two sets are independent -- and the
+    values that are returned match as hex (golden from the reference)."""
+    from paper_1701_08547_b200 import mix as M
+    g = golden("partial_table.json")
+    if not same_sum_semantics(g["meta"]):
+        pytest.skip("goldens captured under a different CPython sum()")
+    full = dict(M.DEFAULT_THROUGHPUT.ipc)
+    seen = set()
+    for row in g["rows"]:
+        drop = {(P.OpClass(c), key) for c, key in row["drop"]}
+        table = M.ThroughputTable({k: v for k, v in full.items() if k not in drop})
+        mx = _mix(P, row["counts"], row["reg_operands"])
+        cc = row["cc"]
+        calls = {"cost": lambda: M.cost_estimate(mx, cc, 1.0, table),
+                 "cycles": lambda: M.category_cycles(mx, cc, table),
+                 "shares": lambda: M.pipeline_utilization(mx, cc, table),
+                 "per_class": lambda: M.per_class_cycles(mx, cc, table)}
+        for name, call in calls.items():
+            want = row[name]
+            if want == "KeyError":
+                with pytest.raises(KeyError):
+                    call()
+                continue
+            got = call()
+            if isinstance(got, dict):
+                got = {c.value: x.hex() for c, x in got.items()}
+            else:
+                got = got.hex()
+            assert got == want, (row, name)
+        seen.add((row["cost"] == "KeyError", row["per_class"] == "KeyError"))
+    assert seen == {(False, False), (True, True), (True, False), (False, True)}
+
+
 def test_k1_random_mixes_golden(P, golden):
     from paper_1701_08547_b200.batch import feature_score
     g = golden("mix.json")

@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 def random_arch(rng, i):
     from paper_1701_08547_b200.arch import ArchSpec, Family
     ws = rng.choice((8, 16, 32, 32, 32, 64))
-    wpb_max = rng.randint(1, 64)
+    wpb_max = rng.randint(1, min(64, 2048 // ws))          # device tables: T <= 2048
     tmax = ws * wpb_max
     wmp = rng.randint(1, min(127, max(1, 4096 // ws)))
     bmp = rng.randint(1, 255)
@@ -49,7 +49,7 @@ def random_config(rng, n_arch=3, n_kern=3):
     archs = tuple(random_arch(rng, i) for i in range(n_arch))
     kernels = []
     for kk in range(n_kern):
-        tc = tuple(sorted(rng.sample(range(32, 2048, 32), rng.randint(1, 12))))   # masks: T < 2048
+        tc = tuple(sorted(rng.sample(range(32, 2049, 32), rng.randint(1, 12))))   # masks: T <= 2048
         if rng.random() < 0.3:
             tc = tuple(rng.sample(tc, len(tc)))                  # unsorted thread dimension
         space = TuningSpace(tc, tuple(rng.sample(range(1, 300), rng.randint(1, 3))),
@@ -229,7 +229,7 @@ def random_big_block_config(rng, n_arch=3, n_kern=2):
     archs = tuple(random_arch(rng, i) for i in range(n_arch))
     kernels = []
     for kk in range(n_kern):
-        tc = tuple(sorted(rng.sample(range(32, 2048, 32), rng.randint(1, 5))))
+        tc = tuple(sorted(rng.sample(range(32, 2049, 32), rng.randint(1, 5))))
         regs = tuple(rng.sample(range(0, 1100), rng.randint(20, 300)))
         smem = tuple(rng.choice((0, 1, 1024, 6145, 49152, 232448, rng.randint(0, 1 << 25)))
                      for _ in range(rng.randint(1, 70)))

@@ -93,13 +93,14 @@ def test_prune_numbers():
 @pytest.mark.parametrize("ai", range(5))
 def test_membership_masks_match_oracle_sets(ai):
     arch = workloads.all_archs()[ai]
-    for tcs in (TuningSpace().thread_counts, (32, 64, 96), (128,), tuple(range(64, 2017, 64))):
+    for tcs in (TuningSpace().thread_counts, (32, 64, 96), (128,), tuple(range(64, 2017, 64)),
+                (2048, 32, 1024, 1984)):
         sp = TuningSpace(thread_counts=tcs)
         st, lo, hi = membership_masks(sp, thread_candidates(arch))
         kept = pyref.static_kept(tcs, set(pyref.thread_candidates(arch)))
         want_lo = set(pyref.rule_kept(kept, 0.0)) if kept else set()
         want_hi = set(pyref.rule_kept(kept, math.inf)) if kept else set()
-        bits = lambda m: {32 * b for b in range(64) if (m >> b) & 1}
+        bits = lambda m: {32 * (b + 1) for b in range(64) if (m >> b) & 1}
         assert bits(st) == set(kept) and bits(lo) == want_lo and bits(hi) == want_hi
 
 
