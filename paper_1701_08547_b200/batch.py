@@ -19,6 +19,7 @@ from dataclasses import dataclass, field
 from typing import Sequence
 
 import numpy as np
+from itertools import chain
 
 from . import _lib
 from .arch import ArchSpec, COST_KEY_OF_MAJOR, pack_archs
@@ -59,6 +60,34 @@ def _to_device(arr: np.ndarray):
     if flat.size:
         t[: flat.size].copy_(torch.from_numpy(flat))
     return t
+
+
+class _DevPtr:
+    """A device address inside a buffer the plan owns (passed to the C ABI)."""
+
+    __slots__ = ("addr",)
+
+    def __init__(self, addr: int):
+        self.addr = addr
+
+    def data_ptr(self) -> int:
+        return self.addr
+
+
+_HOST = None
+
+
+def _host():
+    """The native host module (csrc/occx_host.cpp); raises when it is not built."""
+    global _HOST
+    if _HOST is None:
+        try:
+            from . import _occx_host
+        except ImportError as exc:
+            raise DeviceError("paper_1701_08547_b200/_occx_host is not built; run "
+                              "`python -m paper_1701_08547_b200.build`") from exc
+        _HOST = _occx_host
+    return _HOST
 
 
 def _empty(nbytes: int):
@@ -311,26 +340,33 @@ _CPI_CLASS = {row: cls for cls, row in CPI_ROW.items()}
 def pack_mixes(mixes: Sequence[InstructionMix]) -> np.ndarray:
     """InstructionMix objects -> occx_mix_t rows; first_key = insertion rank."""
     n = len(mixes)
-    counts = np.zeros((n, 16), np.int64)
-    first = np.full((n, 16), U32_MAX, np.int64)
-    regs = np.zeros(n, np.int64)
-    total = np.zeros(n, np.int64)
-    for i, m in enumerate(mixes):
-        row_c, row_f = counts[i], first[i]
-        for rank, (cls, c) in enumerate(m.counts.items()):
-            d = DEVICE_ID[cls]
-            row_c[d] = c
-            row_f[d] = rank
-        regs[i] = m.reg_operands
-        total[i] = m.total_instructions
-    if n and counts.max() > U32_MAX:
-        raise DeviceError("per-class count above 2^32-1")
-    out = np.zeros(n, _lib.MIX)
-    out["counts"] = counts
-    out["first_key"] = first
-    out["reg_operands"] = regs
-    out["n_instr"] = np.minimum(total, U32_MAX)
-    return out
+    # flat (row*16 + device id, count, insertion rank) columns (C-level
+    # iteration over the dicts), one numpy scatter
+    dicts = [m.counts for m in mixes]
+    lens = np.fromiter(map(len, dicts), np.int64, n)
+    ids = np.fromiter(map(DEVICE_ID.__getitem__, chain.from_iterable(dicts)), np.int64)
+    vals = list(chain.from_iterable(d.values() for d in dicts))
+    regs = [m.reg_operands for m in mixes]
+    starts = np.cumsum(lens) - lens
+    rows = np.repeat(np.arange(n, dtype=np.int64), lens)
+    ranks = np.arange(len(ids), dtype=np.int64) - np.repeat(starts, lens)
+    cell = 16 * rows + ids
+    # occx_mix_t as 36 u32 words: counts[16] | first_key[16] | reg_operands
+    # (u64 lo, hi) | n_instr | reserved
+    words = np.zeros((n, 36), np.uint32)
+    words[:, 16:32] = U32_MAX
+    flat = words.reshape(-1)
+    if vals:
+        if max(vals) > U32_MAX:
+            raise DeviceError("per-class count above 2^32-1")
+        cell += 20 * rows                           # row*16+d -> row*36+d
+        flat[cell] = vals
+        flat[cell + 16] = ranks
+    r = np.asarray(regs, np.uint64)
+    words[:, 32] = r & np.uint64(U32_MAX)
+    words[:, 33] = r >> np.uint64(32)
+    words[:, 34] = np.minimum(words[:, :16].sum(axis=1, dtype=np.uint64), U32_MAX)
+    return words.view(_lib.MIX).reshape(n)
 
 
 def _nonneg_ints(vals) -> np.ndarray:
@@ -409,12 +445,14 @@ class FeatureBatch:
 
 
 def feature_records(d_mix, n_mix: int, cols: Sequence[int], cpi: np.ndarray, scale: float,
-                    sum_mode: int = SUM_MODE):
-    """Device-level K1 -> (d_sum, d_feat)."""
+                    sum_mode: int = SUM_MODE, d_sum=None, d_feat=None):
+    """Device-level K1 -> (d_sum, d_feat) (allocated unless given)."""
     h_cols = np.asarray(list(cols) or [0], np.int32)
     h_cpi = np.ascontiguousarray(cpi, np.float64).reshape(4, 16)
-    d_sum = _empty(n_mix * _lib.MIXSUM.itemsize)
-    d_feat = _empty(n_mix * max(len(cols), 1) * _lib.FEAT.itemsize)
+    if d_sum is None:
+        d_sum = _empty(n_mix * _lib.MIXSUM.itemsize)
+    if d_feat is None:
+        d_feat = _empty(n_mix * max(len(cols), 1) * _lib.FEAT.itemsize)
     _lib.check(_lib.load().occx_feature_score(
         _lib.ctx(), _lib.ptr(d_mix), n_mix, _lib.ptr(h_cols), len(cols), _lib.ptr(h_cpi),
         float(scale), sum_mode, _lib.ptr(d_sum), _lib.ptr(d_feat) if cols else None,
@@ -458,19 +496,18 @@ class KernelSpec:
         return len(self.space.unroll_factors) * len(self.space.compiler_flags)
 
 
-@dataclass(slots=True)
-class Ranked:
-    """One entry of a segment's top-k list, decoded from its key."""
+def _ranked_type():
+    try:
+        from ._occx_host import Ranked as R
+    except ImportError:          # the module is required on use (_host()); keep import cheap
+        return None
+    return R
 
-    index: int              # global candidate index
-    config: tuple           # enumerate_space(kernel.space) tuple
-    variant: int
-    arch: int
-    active_warps: int
-    rule_keep: bool
-    static_keep: bool
-    cost_rank: int | None
-    key: int
+
+# One entry of a segment's top-k list, decoded from its key: a C struct
+# sequence (index, config, variant, arch, active_warps, rule_keep,
+# static_keep, cost_rank, key), built by the native decoder.
+Ranked = _ranked_type()
 
 
 @dataclass
@@ -522,103 +559,73 @@ class ScorePlan:
             mixes += list(kern.mixes)
             var_kernel += [ki] * len(kern.mixes)
         self.n_var = len(mixes)
-        # segments: descriptors + value pool + masks.  The value pool of a
-        # kernel's seven dimensions is shared by its n_arch segments.
-        pool_parts: list[np.ndarray] = []
-        n_pool = 0
-        desc = np.zeros(self.n_seg, _lib.SEGDESC)
-        masks = np.zeros((self.n_seg, 3), np.uint64)
-        d_rows: list = []
-        d_offs: list = []
-        d_lens: list = []
-        cands = [thread_candidates(a) for a in self.archs]
-        self.seg_start: list[int] = []
-        self.seg_dims: list[list[tuple]] = []
-        start = 0
-        for ki, kern in enumerate(self.kernels):
+        # segments: descriptors + value pool + masks + variants + mixes,
+        # packed natively (csrc/occx_host.cpp) into one H2D blob.  The value
+        # pool of a kernel's seven dimensions is shared by its n_arch segments.
+        dims_all, self.seg_dims, self.kern_dims = [], [], []
+        for kern in self.kernels:
             sp = kern.space
-            extras = {name.upper(): vals for name, vals in sp.extra}
             names = [n.upper() for n, _ in sp.extra]
             if any(n not in ("REGS", "SMEM") for n in names) or names not in (
                     [], ["REGS"], ["SMEM"], ["REGS", "SMEM"]):
                 raise ValueError("extra dimensions must be REGS and/or SMEM, in that order")
-            regs = extras.get("REGS", (kern.registers_per_thread,))
-            smem = extras.get("SMEM", (kern.static_shared_mem,))
-            dims = [sp.thread_counts, sp.block_counts, sp.unroll_factors, sp.l1_sizes_kb,
-                    sp.compiler_flags, regs, smem]
-            offs, lens = [], []
-            for j, vals in enumerate(dims):
-                offs.append(n_pool)
-                lens.append(len(vals))
-                if j in (0, 1, 5, 6):          # value dims; UIF/PL/CFLAGS by index
-                    arr = _nonneg_ints(vals)
-                    pool_parts.append(np.minimum(arr, U32_MAX).astype(np.uint32))
-                else:
-                    pool_parts.append(np.zeros(len(vals), np.uint32))
-                n_pool += len(vals)
-            size = grid_size(sp)
+            extras = {name.upper(): vals for name, vals in sp.extra}
+            dims_all.append((sp.thread_counts, sp.block_counts, sp.unroll_factors,
+                             sp.l1_sizes_kb, sp.compiler_flags,
+                             extras.get("REGS", (kern.registers_per_thread,)),
+                             extras.get("SMEM", (kern.static_shared_mem,))))
             seg_dims = [tuple(v) for _, v in sp._dimensions()]
-            mask_of: dict = {}                 # archs sharing T* share the masks
-            for a in range(self.n_arch):
-                s = ki * self.n_arch + a
-                d_rows.append((start, size, a, self.var_base[ki]))
-                d_offs.append(offs)
-                d_lens.append(lens)
-                self.seg_start.append(start)
-                self.seg_dims.append(seg_dims)
-                start += size
-                m = mask_of.get(cands[a])
-                if m is None:
-                    m = mask_of[cands[a]] = membership_masks(sp, cands[a])
-                masks[s] = m
-        if d_rows:                             # descriptor columns in one go
-            cols = np.asarray(d_rows, np.uint64)
-            desc["start"], desc["size"] = cols[:, 0], cols[:, 1]
-            desc["arch"], desc["var_base"] = cols[:, 2], cols[:, 3]
-            desc["dim_off"] = np.asarray(d_offs, np.uint32)
-            desc["dim_len"] = np.asarray(d_lens, np.uint32)
-        self.total = start
+            self.kern_dims.append(seg_dims)
+            self.seg_dims += [seg_dims] * self.n_arch
+        blob, offsets, self.total, self.n_pool = _host().pack_plan(
+            dims_all, [len(k.mixes) for k in self.kernels], mixes,
+            [thread_candidates(a) for a in self.archs], DEVICE_ID, DeviceError)
         if self.total > IDX_MASK + 1:
             raise DeviceError("search space above 2^34 candidates")
+        desc = np.frombuffer(blob, _lib.SEGDESC, self.n_seg, offsets[0])
+        self._seg_start_np = desc["start"].astype(np.int64)
+        self.seg_start = self._seg_start_np.tolist()
         self.var_kernel = np.asarray(var_kernel, np.uint32)
         self.mixes = mixes
-        self._seg_start_np = np.asarray(self.seg_start, np.int64)
-        pool = np.concatenate(pool_parts) if pool_parts else np.zeros(1, np.uint32)
-        self.n_pool = max(len(pool), 1)
-        # one H2D copy of the whole space description, carved into views
-        parts = [desc.view(np.uint8).ravel(), pool.view(np.uint8).ravel(),
-                 masks.view(np.uint8).ravel(), self.var_kernel.view(np.uint8).ravel(),
-                 pack_mixes(mixes).view(np.uint8).ravel()]
-        offsets, total_b = [], 0
-        for part in parts:
-            offsets.append(total_b)
-            total_b += -(-max(part.size, 1) // 256) * 256
-        blob = np.zeros(total_b, np.uint8)
-        for o, part in zip(offsets, parts):
-            blob[o:o + part.size] = part
-        self._d_blob = _to_device(blob)
-        views = [self._d_blob[o:] for o in offsets]
-        self.d_desc, self.d_pool, self.d_masks, self.d_var_kernel, d_mix = views
+        self._blob, self._offsets = blob, offsets
         # bytes this plan copied host -> device (the space description; the
         # arch rows and CPI table travel in the kernel parameter blocks)
-        self.h2d_bytes = int(blob.nbytes + self.h_archs.nbytes + 4 * 16 * 8)
-        # K1 on device, then the feature table
-        cols = [int(a["cost_key"]) for a in self.h_archs]
-        self.d_sum, self.d_feat = feature_records(d_mix, self.n_var, cols, table.cpi_matrix(),
-                                                  scale)
-        self.d_vtab = _empty(self.n_var * self.n_arch * _lib.VENT.itemsize)
-        _lib.check(_lib.load().occx_build_vtab(
-            _lib.ctx(), _lib.ptr(self.d_sum), _lib.ptr(self.d_feat), self.n_var, self.n_arch,
-            _lib.ptr(self.d_var_kernel), _lib.ptr(self.d_masks),
-            _lib.ptr(self.d_vtab), _lib.stream_ptr()), "occx_build_vtab")
+        self.h2d_bytes = int(len(blob) + self.h_archs.nbytes + 4 * 16 * 8)
+        # one device buffer: the space description (H2D) | K1 sums | K1
+        # features | feature table | K2 workspace
         ws = ctypes_u64()
         _lib.check(_lib.load().occx_score_workspace_bytes(self._ctx, self.n_seg, k,
                                                           ws.ref()), "workspace")
         self.ws_bytes = ws.value
         # per-CTA partial tables K2 leaves in the workspace (score_partials)
         self.grid_lists = self.ws_bytes // (self.n_seg * k * 8)
-        self.d_ws = _empty(self.ws_bytes)
-        self.masks = masks
+        n_cell = self.n_var * self.n_arch
+        parts = [len(blob), self.n_var * _lib.MIXSUM.itemsize, n_cell * _lib.FEAT.itemsize,
+                 n_cell * _lib.VENT.itemsize, self.ws_bytes]
+        offs, total_b = [], 0
+        for nb in parts:
+            offs.append(total_b)
+            total_b += -(-max(nb, 1) // 256) * 256
+        self._d_buf = _empty(total_b)
+        self._d_buf[:len(blob)].copy_(_torch().frombuffer(blob, dtype=_torch().uint8))
+        base = self._d_buf.data_ptr()
+        self.d_desc, self.d_pool, self.d_masks, self.d_var_kernel, d_mix = (
+            _DevPtr(base + o) for o in offsets)
+        self.d_sum, self.d_feat, self.d_vtab, self.d_ws = (_DevPtr(base + o) for o in offs[1:])
+        # K1 on device, then the feature table
+        cols = [int(a["cost_key"]) for a in self.h_archs]
+        feature_records(d_mix, self.n_var, cols, table.cpi_matrix(), scale,
+                        d_sum=self.d_sum, d_feat=self.d_feat)
+        _lib.check(_lib.load().occx_build_vtab(
+            _lib.ctx(), _lib.ptr(self.d_sum), _lib.ptr(self.d_feat), self.n_var, self.n_arch,
+            _lib.ptr(self.d_var_kernel), _lib.ptr(self.d_masks),
+            _lib.ptr(self.d_vtab), _lib.stream_ptr()), "occx_build_vtab")
+
+    @property
+    def masks(self) -> np.ndarray:
+        """[n_seg, 3] u64 (static, rule-lower, rule-upper) membership masks."""
+        o = self._offsets[2]
+        return np.frombuffer(self._blob, np.uint64, 3 * self.n_seg, o).reshape(self.n_seg, 3)
 
     # -- candidates ---------------------------------------------------------
     def generate(self, begin: int = 0, n: int | None = None, out=None):
@@ -732,68 +739,19 @@ class ScorePlan:
             digits.append(vals[r])
         return s, tuple(reversed(digits))
 
-    def decode_tables(self) -> list:
-        """Key-independent part of decode (per kernel: its dimensions as
-        object arrays for fancy indexing); cached on the plan, so the API
-        can build it while the GPU scores."""
-        tabs = getattr(self, "_decode_tabs", None)
-        if tabs is None:
-            tabs = []
-            for ki in range(len(self.kernels)):
-                dims = self.seg_dims[ki * self.n_arch]
-                cols = []
-                for vals_in in dims:
-                    vals = np.empty(len(vals_in), dtype=object)
-                    for i_v, v in enumerate(vals_in):           # values kept as given
-                        vals[i_v] = v
-                    cols.append(vals)
-                tabs.append((dims, cols))
-            self._decode_tabs = tabs
-        return tabs
-
     def decode(self, keys) -> list[SegmentTopK]:
-        """[n_seg, k] keys -> per-segment Ranked entries (host).  The key
-        fields are unpacked with numpy; each entry's space tuple comes from
-        its mixed-radix digits (enumerate_space order, last dimension
-        fastest).  Indices of weak-scaling copies are taken modulo total."""
-        tabs = self.decode_tables()
-        keys = np.asarray(keys.cpu().numpy() if hasattr(keys, "cpu") else keys).view(np.uint64)
-        keys = keys.reshape(self.n_seg, self.k)
-        idx = (np.uint64(IDX_MASK) - (keys & np.uint64(IDX_MASK))).astype(np.int64)
-        local = (idx % self.total) - self._seg_start_np[:, None]
-        aw = ((keys >> np.uint64(54)) & np.uint64(0x7F)).astype(np.int64).tolist()
-        rk = ((keys >> np.uint64(34)) & np.uint64(0xFFFFF)).astype(np.int64).tolist()
-        rule = ((keys >> np.uint64(62)) & np.uint64(1)).astype(bool).tolist()
-        stat = ((keys >> np.uint64(61)) & np.uint64(1)).astype(bool).tolist()
-        nz = (keys != 0).tolist()
-        idx_l, keys_l = idx.tolist(), keys.tolist()
-        out = []
-        na, k = self.n_arch, self.k
-        for ki, kern in enumerate(self.kernels):
-            # the kernel's n_arch segments share its dimensions: digits of all
-            # their entries at once (numpy), configs zipped into tuples in C
-            dims, vcols = tabs[ki]
-            nd = len(dims)
-            rem = local[ki * na:(ki + 1) * na].reshape(-1).copy()
-            rem[rem < 0] = 0                                    # empty slots (key 0)
-            digs = [None] * nd
-            for d in range(nd - 1, -1, -1):
-                rem, digs[d] = np.divmod(rem, len(dims[d]))
-            configs = list(zip(*[vcols[d][digs[d]] for d in range(nd)]))
-            variants = (self.var_base[ki] + digs[2] * len(dims[4]) + digs[4]).tolist()
-            for a in range(na):
-                s = ki * na + a
-                entries = []
-                for j in range(k):
-                    if not nz[s][j]:
-                        continue
-                    f = a * k + j
-                    rbits = rk[s][j]
-                    entries.append(Ranked(
-                        idx_l[s][j], configs[f], variants[f], a, aw[s][j], rule[s][j],
-                        stat[s][j], ((1 << 20) - 1 - rbits) if rbits else None, keys_l[s][j]))
-                out.append(SegmentTopK(kern.name, self.archs[a].name, entries))
-        return out
+        """[n_seg, k] keys -> per-segment Ranked entries (host, native: the
+        key fields, the global index -> enumerate_space digits, last
+        dimension fastest, ref tuning.py:70-77).  Indices of weak-scaling
+        copies are taken modulo total."""
+        keys = np.asarray(keys.cpu().numpy() if hasattr(keys, "cpu") else keys)
+        keys = np.ascontiguousarray(keys).view(np.uint64).reshape(self.n_seg, self.k)
+        segs = _host().decode(keys, self.n_arch, self.k, self.total, self.seg_start,
+                              self.kern_dims, self.var_base)
+        names = [a.name for a in self.archs]
+        na = self.n_arch
+        return [SegmentTopK(self.kernels[s // na].name, names[s % na], e)
+                for s, e in enumerate(segs)]
 
 
 class ctypes_u64:
@@ -820,5 +778,4 @@ def score_space(kernels: Sequence[KernelSpec], archs: Sequence[ArchSpec],
     ``prune=False`` evaluates every key (no exact block skipping)."""
     plan = ScorePlan(kernels, archs, mode, k)
     keys = plan.score_implicit(prune=prune)
-    plan.decode_tables()               # host work while the GPU scores
     return plan.decode(keys)

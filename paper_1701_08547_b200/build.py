@@ -22,6 +22,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-
           "-cudart", "shared"]
 CXX = os.environ.get("CXX", "g++")
 CXX_SOURCES = {"occx_sass.cpp": []}     # host-only C++ (tokenizer)
+# + csrc/occx_host.cpp: CPython extension _occx_host (plan packing, decoding)
 SOURCES = {
     "occx_capi.cu": [],
     "occx_score.cu": [],
@@ -75,6 +76,17 @@ def build(verbose: bool = False, timing: bool = False) -> str:
             failed.append(src)
     if failed:
         raise RuntimeError(f"compile failed on {', '.join(failed)}")
+    if not timing:        # the native host module (CPython extension, csrc/occx_host.cpp)
+        import sysconfig
+        ext = os.path.join(HERE, "_occx_host" + sysconfig.get_config_var("EXT_SUFFIX"))
+        src = os.path.join(CSRC, "occx_host.cpp")
+        if _stale(ext, [src, __file__]):
+            r = subprocess.run([CXX, "-O2", "-std=c++17", "-fPIC", "-shared", "-Wall",
+                                "-I" + sysconfig.get_paths()["include"], src, "-o", ext],
+                               capture_output=True, text=True)
+            if r.returncode:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError("compile failed on occx_host.cpp")
     if _stale(out, objs):
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", out, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)

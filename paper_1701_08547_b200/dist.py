@@ -69,7 +69,6 @@ def score_space_multi(kernels, archs, mode="corrected", k: int = 16, group=None,
         local = plan.score_implicit(begin, end - begin, prune=prune)
     else:
         raise ValueError("scaling must be 'strong' or 'weak'")
-    plan.decode_tables()               # host work while the GPU scores
     if world > 1:
         if gather_on_host:
             local = allgather_merge(local.cpu(), lambda g: plan.merge(g.cuda(), g.shape[0]),

@@ -194,6 +194,7 @@ def test_decode_matches_locate_on_random_keys():
             dims.append(d)
             st += size
     plan.seg_start, plan.seg_dims, plan.total, plan.var_base = starts, dims, st, vb
+    plan.kern_dims = dims[::plan.n_arch]
     plan._seg_start_np = np.asarray(starts, np.int64)
     rng = np.random.default_rng(3)
     keys = np.zeros((plan.n_seg, plan.k), np.uint64)
@@ -213,3 +214,117 @@ def test_decode_matches_locate_on_random_keys():
                 sp.compiler_flags.index(cfg_t[4])
             assert e.variant == want_v and e.cost_rank == (1 << 20) - 1 - 7
     assert sum(len(s.entries) for s in plan.decode(keys)) == int((keys != 0).sum())
+
+
+def _py_pack(kernels, archs):
+    """Python restatement of the plan blob parts (descriptors, pool, masks,
+    var_kernel, mixes) for the native packer."""
+    import numpy as np
+    from paper_1701_08547_b200.batch import pack_mixes
+    from paper_1701_08547_b200.tuning import grid_size
+    pool, rows, masks, vk, mixes = [], [], [], [], []
+    start = 0
+    for ki, kern in enumerate(kernels):
+        sp = kern.space
+        ex = {n.upper(): v for n, v in sp.extra}
+        dims = [sp.thread_counts, sp.block_counts, sp.unroll_factors, sp.l1_sizes_kb,
+                sp.compiler_flags, ex.get("REGS", (kern.registers_per_thread,)),
+                ex.get("SMEM", (kern.static_shared_mem,))]
+        offs, lens = [], []
+        for j, vals in enumerate(dims):
+            offs.append(len(pool))
+            lens.append(len(vals))
+            pool += [min(int(v), 2**32 - 1) if j in (0, 1, 5, 6) else 0 for v in vals]
+        size = grid_size(sp)
+        for a, arch in enumerate(archs):
+            rows.append((start, size, a, len(mixes), offs, lens))
+            masks.append(membership_masks(sp, thread_candidates(arch)))
+            start += size
+        vk += [ki] * len(kern.mixes)
+        mixes += list(kern.mixes)
+    return rows, np.asarray(pool, np.uint32), np.asarray(masks, np.uint64).reshape(-1, 3), \
+        np.asarray(vk, np.uint32), pack_mixes(mixes), start
+
+
+def _native_pack(kernels, archs):
+    from paper_1701_08547_b200.batch import DeviceError, _host
+    from paper_1701_08547_b200.mix import DEVICE_ID
+    dims = []
+    for kern in kernels:
+        sp = kern.space
+        ex = {n.upper(): v for n, v in sp.extra}
+        dims.append((sp.thread_counts, sp.block_counts, sp.unroll_factors, sp.l1_sizes_kb,
+                     sp.compiler_flags, ex.get("REGS", (kern.registers_per_thread,)),
+                     ex.get("SMEM", (kern.static_shared_mem,))))
+    mixes = [m for k in kernels for m in k.mixes]
+    return _host().pack_plan(dims, [len(k.mixes) for k in kernels], mixes,
+                             [thread_candidates(a) for a in archs], DEVICE_ID, DeviceError)
+
+
+def _check_native_pack(kernels, archs):
+    import numpy as np
+    from paper_1701_08547_b200 import _lib
+    rows, pool, masks, vk, mix, total = _py_pack(kernels, archs)
+    blob, offs, n_total, n_pool = _native_pack(kernels, archs)
+    assert n_total == total and n_pool == max(len(pool), 1)
+    n_seg = len(rows)
+    desc = np.frombuffer(blob, _lib.SEGDESC, n_seg, offs[0])
+    for d, (st, size, a, vb, o, ln) in zip(desc, rows):
+        assert (int(d["start"]), int(d["size"]), int(d["arch"]), int(d["var_base"])) == (st, size, a, vb)
+        assert d["dim_off"].tolist() == o and d["dim_len"].tolist() == ln
+    assert np.array_equal(np.frombuffer(blob, np.uint32, len(pool), offs[1]), pool)
+    assert np.array_equal(np.frombuffer(blob, np.uint64, 3 * n_seg, offs[2]).reshape(-1, 3), masks)
+    assert np.array_equal(np.frombuffer(blob, np.uint32, len(vk), offs[3]), vk)
+    assert np.frombuffer(blob, np.uint8, mix.nbytes, offs[4]).tobytes() == mix.tobytes()
+
+
+def test_native_pack_plan_matches_python_restatement():
+    """csrc/occx_host.cpp pack_plan == the Python packing (membership_masks,
+    value pool clamps, descriptor rows, pack_mixes) on the workloads and on
+    spaces with duplicate / unsorted / numpy-int / huge thread and value
+    entries."""
+    import random
+    import numpy as np
+    from paper_1701_08547_b200 import workloads
+    from paper_1701_08547_b200.batch import KernelSpec
+    from paper_1701_08547_b200.mix import COUNTABLE, InstructionMix
+    for cfg in (workloads.config1(), workloads.config2(), workloads.config4(), workloads.config5()):
+        _check_native_pack(cfg.kernels, cfg.archs)
+    rng = random.Random(5)
+    archs = workloads.all_archs()
+    for _ in range(60):
+        kernels = []
+        for kk in range(rng.randint(1, 4)):
+            tc = [rng.choice(range(32, 2049, 32)) for _ in range(rng.randint(1, 14))]
+            tc += rng.sample(tc, min(len(tc), rng.randint(0, 3)))          # duplicates
+            if rng.random() < 0.3:
+                tc = [np.int64(t) for t in tc]
+            regs = tuple(rng.choice((0, 27, 255, 300, 2**40)) for _ in range(rng.randint(1, 4)))
+            space = TuningSpace(tuple(tc), tuple(rng.sample(range(1, 300), rng.randint(1, 3))),
+                                (1, 2)[:rng.randint(1, 2)], (16,), ("", "-use_fast_math"),
+                                extra=(("REGS", regs),) if rng.random() < 0.7 else ())
+            n_var = len(space.unroll_factors) * len(space.compiler_flags)
+            mixes = tuple(InstructionMix({c: rng.randint(0, 2**32 - 1) for c in
+                                          rng.sample(COUNTABLE, rng.randint(0, 8))},
+                                         rng.randint(0, 2**62)) for _ in range(n_var))
+            kernels.append(KernelSpec(f"k{kk}", space, mixes, rng.randint(0, 64),
+                                      rng.randint(0, 49152)))
+        _check_native_pack(kernels, rng.sample(archs, rng.randint(1, 5)))
+
+
+def test_native_pack_plan_errors():
+    from paper_1701_08547_b200 import workloads
+    from paper_1701_08547_b200.batch import DeviceError, KernelSpec
+    from paper_1701_08547_b200.mix import InstructionMix, OpClass
+    arch = workloads.all_archs()[:1]
+    two = (InstructionMix(), InstructionMix())
+    sp = TuningSpace((64, 128), (1,), (1,), (16,), ("", "-f"), extra=(("REGS", (1, -3)),))
+    with pytest.raises(ValueError, match="non-negative ints"):
+        _native_pack([KernelSpec("a", sp, two)], arch)
+    sp = TuningSpace((64,), (1.5,), (1,), (16,), ("", "-f"))
+    with pytest.raises(ValueError, match="non-negative ints"):
+        _native_pack([KernelSpec("a", sp, two)], arch)
+    sp = TuningSpace((64,), (1,), (1,), (16,), ("", "-f"))
+    big = (InstructionMix({OpClass.FP32: 2**32}), InstructionMix())
+    with pytest.raises(DeviceError, match="above 2\\^32-1"):
+        _native_pack([KernelSpec("a", sp, big)], arch)
