@@ -241,14 +241,10 @@ def cpu_aggregate_baseline(n_kernels: int = 16000):
                       f"(wall {wall:.2f} s incl. input decode)"}
 
 
-def secondary_config3(hbm_peak: float):
-    """K0 over the 100k-kernel corpus (config 3): instructions/s and HBM
-    roofline (4 B/instruction + 8 B offset + 144 B output per kernel)."""
+def _k0_time(c, rec, lut, reps: int = 10) -> float:
+    """Median K0 time (CUDA events, L2 flushed before every launch)."""
     import torch
-    from paper_1701_08547_b200 import _lib, batch, workloads
-    c = workloads.make_corpus(100_000)
-    rec = workloads.corpus_records(c)
-    lut = workloads.corpus_signature_lut()
+    from paper_1701_08547_b200 import _lib, batch
     d_rec, d_off = batch._to_device(rec), batch._to_device(c.offsets)
     d_lut = batch._to_device(lut)
     out = batch._empty(c.n_kernels * _lib.MIX.itemsize)
@@ -256,7 +252,7 @@ def secondary_config3(hbm_peak: float):
     for _ in range(3):
         batch.mix_reduce(d_rec, d_off, c.n_kernels, d_lut, len(lut), d_out=out)
     ts = []
-    for _ in range(10):
+    for _ in range(reps):
         flush.fill_(1)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -264,17 +260,216 @@ def secondary_config3(hbm_peak: float):
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
-    ms = statistics.median(ts)
+    return statistics.median(ts)
+
+
+def secondary_config3(hbm_peak: float):
+    """K0 over the 100k-kernel corpus (config 3): instructions/s and HBM
+    roofline (4 B/instruction + 8 B offset + 144 B output per kernel).
+    Headline input: class records (the record's id field holds classify()
+    of its signature, as the tokenizer emits them, ``tokenize(text,
+    table)``), reduced with the 15-entry identity class table; the
+    signature-id records with the 14,415-entry signature table beside it."""
+    from paper_1701_08547_b200 import batch, workloads
+    c = workloads.make_corpus(100_000)
+    rec = workloads.corpus_records(c)
+    lut = workloads.corpus_signature_lut()
+    ms = _k0_time(c, batch.classify_records(rec, lut), batch.CLASS_LUT)
+    ms_sig = _k0_time(c, rec, lut)
     byts = 4 * c.n_instr + 8 * (c.n_kernels + 1) + 144 * c.n_kernels
     gbs = byts / (ms / 1e3) / 1e9
     return {"workload": "config3-100k-kernel-sass-corpus", "kernels": c.n_kernels,
             "instructions": c.n_instr, "value": c.n_instr / (ms / 1e3),
             "unit": "instructions/s", "kernels_per_s": c.n_kernels / (ms / 1e3),
-            "ms": ms, "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak,
-                                   "unit": "GB/s", "frac": gbs / hbm_peak,
-                                   "algorithmic_bytes": byts},
+            "ms": ms, "records": "class records (identity class table)",
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": gbs / hbm_peak, "algorithmic_bytes": byts},
+            "signature_records": {"ms": ms_sig, "value": c.n_instr / (ms_sig / 1e3),
+                                  "frac": byts / (ms_sig / 1e3) / 1e9 / hbm_peak,
+                                  "note": "signature-id records, 14,415-entry class table"},
             "l2": "512 MB buffer written between launches (flush)",
             "cpu_baseline": cpu_aggregate_baseline()}
+
+
+# ---------------------------------------------------------------------------
+# acceptance 7a: Kd over the reference's full occupancy sweep
+# ---------------------------------------------------------------------------
+
+REF_7A_SECONDS = 6.9     # /root/reference/pkg/test_output.txt:231 (Python 3.10.12, 1 process)
+
+
+def _sweep_7a():
+    """The launches of the reference's acceptance criterion 7a
+    (pkg/tests/test_acceptance.py:148-166): 4 builtin archs x T 32..1024
+    step 32 x R 0..255 x S 0..49152 step 1024 = 1,605,632 occupancy() calls."""
+    import numpy as np
+    from paper_1701_08547_b200.arch import BUILTIN_ARCHS, Family
+    archs = [BUILTIN_ARCHS[f] for f in (Family.FERMI, Family.KEPLER, Family.MAXWELL,
+                                        Family.PASCAL)]
+    T, R, S = np.meshgrid(np.arange(32, 1025, 32), np.arange(256), np.arange(0, 49153, 1024),
+                          indexing="ij")
+    one = np.stack([T.ravel(), R.ravel(), S.ravel()], axis=1)
+    launches = np.tile(one, (len(archs), 1))
+    arch_index = np.repeat(np.arange(len(archs)), len(one))
+    return archs, launches, arch_index
+
+
+def _cpu_occ_worker(args):
+    from oracle import pyref
+    archs, rows = args
+    t0 = time.perf_counter()
+    for a, t, r, s in rows:
+        pyref.occupancy(archs[a], t, r, s)
+    return time.perf_counter() - t0, len(rows)
+
+
+def secondary_acceptance_7a(hbm_peak: float, reps: int = 20):
+    """Kd (occx_occupancy_batch: every OccupancyResult field) over the
+    acceptance-7a sweep: device-level (records resident, L2 flushed) and end
+    to end through occupancy_batch() (host launches in, columnar results
+    out, the criterion's bounds checked), against the reference's recorded
+    6.9 s and the Python restatement on all host cores."""
+    import multiprocessing as mp
+    import numpy as np
+    import torch
+    from paper_1701_08547_b200 import _lib, batch
+    archs, launches, arch_index = _sweep_7a()
+    n = len(launches)
+    rec = batch.pack_launches(launches, arch_index)
+    d_rec = batch._to_device(rec)
+    out = batch._empty(n * _lib.OCC.itemsize)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        batch.occupancy_records(archs, d_rec, n, d_out=out)
+    ts = []
+    for _ in range(reps):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        batch.occupancy_records(archs, d_rec, n, d_out=out)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = statistics.median(ts)
+    byts = n * (16 + _lib.OCC.itemsize)
+    max_w = np.asarray([a.max_warps_per_mp for a in archs])[arch_index]
+
+    def api():
+        res = batch.occupancy_batch(archs, launches, arch_index=arch_index)
+        occ = res.occupancy
+        assert ((occ >= 0.0) & (occ <= 1.0)).all() and (res.active_warps <= max_w).all()
+        return res
+    api()
+    e2e = []
+    for _ in range(5):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        api()
+        e2e.append(time.perf_counter() - t0)
+    e2e_s = statistics.median(e2e)
+    procs = len(os.sched_getaffinity(0))
+    rows = np.column_stack([arch_index, launches])[::8].tolist()
+    with mp.get_context("fork").Pool(procs) as pool:
+        t0 = time.perf_counter()
+        res = pool.map(_cpu_occ_worker, [(archs, rows[i::procs]) for i in range(procs)])
+        wall = time.perf_counter() - t0
+    cpu_n = sum(r[1] for r in res)
+    return {"workload": "acceptance-7a occupancy sweep (4 archs x 32 T x 256 R x 49 S)",
+            "kernel": "occ_dump_kernel (Kd)", "launches": n, "ms": ms,
+            "value": n / (ms / 1e3), "unit": "occupancy() results/s",
+            "roofline": {"bound": "hbm", "achieved": byts / (ms / 1e3) / 1e9, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": byts / (ms / 1e3) / 1e9 / hbm_peak,
+                         "algorithmic_bytes": byts,
+                         "note": "16 B record in + 32 B occx_occ_t out per launch; 77 MB per "
+                                 "call, so launch and ramp dominate"},
+            "e2e": {"seconds": e2e_s, "value": n / e2e_s, "unit": "occupancy() results/s",
+                    "h2d_bytes": int(rec.nbytes), "d2h_bytes": n * _lib.OCC.itemsize,
+                    "path": "occupancy_batch(): pack (T, R, S) -> H2D -> Kd -> D2H -> "
+                            "columnar OccupancyResult batch; criterion 7a bounds checked"},
+            "reference_recorded": {"seconds": REF_7A_SECONDS, "value": n / REF_7A_SECONDS,
+                                   "source": "/root/reference/pkg/test_output.txt:231 "
+                                             "(Python 3.10.12, one process)"},
+            "cpu_baseline": {"value": cpu_n / wall, "unit": "occupancy() results/s",
+                             "cores": procs, "kind": "port",
+                             "sample": f"{cpu_n} launches (every 8th of the sweep), "
+                                       f"oracle/pyref.occupancy, {procs} processes, {wall:.2f} s"}}
+
+
+# ---------------------------------------------------------------------------
+# config 3 end to end: listing text -> native tokenizer -> K0 -> mixes
+# ---------------------------------------------------------------------------
+
+def _corpus_text_part(args):
+    k0, k1 = args
+    from paper_1701_08547_b200 import workloads
+    c = workloads.make_corpus(k1 - k0, first=k0)
+    return workloads.corpus_text(c).replace("Function : kern_", f"Function : k{k0}_")
+
+
+def _cpu_parse_aggregate_worker(text):
+    """The CPU path: parse_disassembly (paper_1701_08547_b200/listing.py, the
+    Python restatement of occmix/sass.py:300-339, pinned to 4,000
+    reference-parsed listings by tests/test_listing.py) + oracle/pyref.aggregate."""
+    from oracle import pyref
+    from paper_1701_08547_b200.listing import parse_disassembly
+    from paper_1701_08547_b200.mix import DEFAULT_OPCLASSES
+    table = {k: v.value for k, v in DEFAULT_OPCLASSES.items()}
+    t0 = time.perf_counter()
+    fns = parse_disassembly(text)
+    t1 = time.perf_counter()
+    for _, instrs in fns:
+        pyref.aggregate([(i.opcode, i.modifiers, i.predicate is not None,
+                          i.register_operand_count) for i in instrs], table)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t0, sum(len(i) for _, i in fns), text.count("\n")
+
+
+def secondary_config3_e2e(n_kernels: int = 1000, reps: int = 5):
+    """Config 3 from text: a listing of the corpus's first ``n_kernels``
+    kernels (reference grammar) -> sass.aggregate_text() = native tokenizer
+    (class records) -> H2D -> K0 -> D2H -> [(name, InstructionMix)].  Also
+    the tokenizer alone (lines/s).  CPU path: parse_disassembly + aggregate
+    per function on all host cores."""
+    import multiprocessing as mp
+    from paper_1701_08547_b200 import sass
+    from paper_1701_08547_b200.mix import DEFAULT_OPCLASSES
+    procs = len(os.sched_getaffinity(0))
+    step = max(1, n_kernels // procs)
+    bounds = [(k, min(k + step, n_kernels)) for k in range(0, n_kernels, step)]
+    with mp.get_context("fork").Pool(procs) as pool:
+        parts = pool.map(_corpus_text_part, bounds)
+    text = "".join(parts)
+    lines = text.count("\n")
+    sass.aggregate_text(text)                    # warm (library, allocator)
+    tok, e2e = [], []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        r = sass.tokenize(text, table=DEFAULT_OPCLASSES)
+        tok.append(time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        mixes = sass.aggregate_text(text)
+        e2e.append(time.perf_counter() - t0)
+    n_instr = len(r.records)
+    assert len(mixes) == n_kernels
+    tok_s, e2e_s = statistics.median(tok), statistics.median(e2e)
+    with mp.get_context("fork").Pool(procs) as pool:
+        t0 = time.perf_counter()
+        res = pool.map(_cpu_parse_aggregate_worker, parts)
+        wall = time.perf_counter() - t0
+    parse_busy = max(x[0] for x in res)
+    return {"workload": f"config-3 corpus listing, first {n_kernels} kernels "
+                        f"({lines} lines, {len(text) / 1e6:.1f} MB)",
+            "instructions": n_instr,
+            "e2e": {"seconds": e2e_s, "value": n_instr / e2e_s, "unit": "instructions/s",
+                    "path": "sass.aggregate_text(): UTF-8 encode -> native tokenizer "
+                            "(threaded, class records) -> H2D -> K0 -> D2H -> InstructionMix"},
+            "tokenizer": {"seconds": tok_s, "value": lines / tok_s, "unit": "lines/s",
+                          "threads": min(procs, 32)},
+            "cpu_baseline": {"value": n_instr / wall, "unit": "instructions/s", "cores": procs,
+                             "kind": "port", "lines_per_s_parse": lines / parse_busy,
+                             "sample": f"the same {n_kernels}-kernel listing split by function "
+                                       f"over {procs} processes: listing.parse_disassembly + "
+                                       f"oracle/pyref.aggregate, {wall:.2f} s wall"}}
 
 
 def secondary_records(name: str, mode: str, hbm_peak: float, steps: int = 20):
@@ -300,7 +495,8 @@ def secondary_records(name: str, mode: str, hbm_peak: float, steps: int = 20):
     return {"workload": cfg.name, "candidates": plan.total, "ms": ms,
             "value": plan.total / (ms / 1e3), "unit": UNIT,
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": gbs / hbm_peak}}
+                         "frac": gbs / hbm_peak},
+            "cpu_baseline": cpu_reference(name, mode, 1_000_000)}
 
 
 def secondary_suggest(mode: str, n_kernels: int = 100_000, steps: int = 20):
@@ -716,6 +912,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_secondary:
         secondary = {}
         for name, fn in (("config3_mix_reduce", lambda: secondary_config3(hbm_peak)),
+                         ("config3_text_e2e", lambda: secondary_config3_e2e()),
+                         ("acceptance_7a_occupancy", lambda: secondary_acceptance_7a(hbm_peak)),
                          ("implicit_grid_score_space", lambda: secondary_space_api(cfg, args.mode)),
                          ("config4_records", lambda: secondary_records("config4", args.mode, hbm_peak)),
                          ("suggest_100k_kernels", lambda: secondary_suggest(args.mode)),

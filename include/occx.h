@@ -61,6 +61,7 @@ typedef enum occx_mode { OCCX_MODE_CORRECTED = 0, OCCX_MODE_VERBATIM = 1 } occx_
  * one slice per warp per stage.  Default 0: TMA, two slices.             */
 #define OCCX_CTX_K2_FEED_LDG 0x1u
 #define OCCX_CTX_K2_ONE_SLICE 0x2u
+#define OCCX_CTX_K2_NO_STEAL 0x4u  /* record scorer: static chunks, no tile stealing */
 
 /* occx_score_space flags.  EVERY_KEY: evaluate every candidate's key (no
  * block-bound pruning); the top-k is the same either way.               */
@@ -251,9 +252,13 @@ int occx_build_vtab(const occx_ctx* ctx, const occx_mixsum_t* d_sum,
  * d_topk[n_seg][k].  Workspace size from occx_score_workspace_bytes.
  * `variant`/`arch` out of range -> candidate excluded.  d_topk == NULL
  * stops after K2: the per-CTA tables stay in d_ws as
- * [occx_score_workspace_bytes / (n_seg*k*8)][n_seg][k] for occx_topk_merge. */
+ * [occx_score_lists(ctx)][n_seg][k] for occx_topk_merge.  The workspace
+ * ends in a scheduler block (the record scorer's per-CTA tile counters,
+ * a multiple of 256 bytes): it must be zero before the first call, and
+ * every call leaves it zero.                                             */
 int occx_score_workspace_bytes(const occx_ctx* ctx, uint32_t n_seg, uint32_t k,
                                uint64_t* bytes);
+int occx_score_lists(const occx_ctx* ctx);
 int occx_score_topk(const occx_ctx* ctx, const occx_arch_t* h_archs, int n_arch,
                     const occx_cand_t* d_cand, uint64_t n, uint64_t index_base,
                     int mode, const occx_vent_t* d_vtab, uint32_t n_var,
@@ -315,6 +320,11 @@ const char* occx_sass_kernel_name(const occx_sass* r, uint32_t k);
 uint32_t occx_sass_n_sigs(const occx_sass* r);
 const char* occx_sass_signature(const occx_sass* r, uint32_t i);
 const char* occx_sass_error_text(const occx_sass* r);
+/* Rewrite the records in place with class ids instead of signature ids
+ * (sig_class[n_sig]: classify() per interned signature, mix.py:176-187;
+ * values <= 14): "class records" for occx_mix_reduce with the identity
+ * class table (n_sig = 15).                                              */
+int occx_sass_classify(occx_sass* r, const uint8_t* sig_class, uint32_t n_sig);
 void occx_sass_free(occx_sass* r);
 
 #ifdef __cplusplus

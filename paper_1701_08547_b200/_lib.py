@@ -66,6 +66,7 @@ SIGNATURES = {
     "occx_feature_score": ([_P, _P, _U32, _P, _U32, _P, _D, _I, _P, _P, _P], _I),
     "occx_build_vtab": ([_P, _P, _P, _U32, _U32, _P, _P, _P, _P], _I),
     "occx_score_workspace_bytes": ([_P, _U32, _U32, _P], _I),
+    "occx_score_lists": ([_P], _I),
     "occx_score_topk": ([_P, _P, _I, _P, _U64, _U64, _I, _P, _U32, _U32, _U32, _P, _U64,
                          _P, _P], _I),
     "occx_topk_merge": ([_P, _P, _U32, _U32, _U32, _P, _P], _I),
@@ -81,6 +82,7 @@ SIGNATURES = {
     "occx_sass_signature": ([_P, _U32], ctypes.c_char_p),
     "occx_sass_error_text": ([_P], ctypes.c_char_p),
     "occx_sass_free": ([_P], None),
+    "occx_sass_classify": ([_P, _P, _U32], _I),
     "occx_score_space": ([_P, _P, _I, _P, _U32, _P, _U32, _U64, _U64, _U64, _I, _U32, _P, _U32,
                           _U32, _U32, _P, _U64, _P, _P], _I),
 }
@@ -126,6 +128,7 @@ def check(status: int, what: str) -> None:
 # context options (include/occx.h): implementation choices, same results
 CTX_K2_FEED_LDG = 0x1
 CTX_K2_ONE_SLICE = 0x2
+CTX_K2_NO_STEAL = 0x4
 SCORE_EVERY_KEY = 0x1           # occx_score_space flag: no block-bound pruning
 
 _ctx: dict[tuple[int, int], int] = {}

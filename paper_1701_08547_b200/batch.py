@@ -259,6 +259,19 @@ def suggest_batch(requests, mode: Mode = Mode.CORRECTED,
 # K0: aggregate
 # ---------------------------------------------------------------------------
 
+# Identity class table: K0 over "class records" (the record's 16-bit id field
+# holds classify() of its signature, computed once per distinct signature on
+# the host).  A 15-entry table keeps every K0 class lookup conflict-free.
+CLASS_LUT = np.arange(15, dtype=np.uint8)
+
+
+def classify_records(records: np.ndarray, sig_class: np.ndarray) -> np.ndarray:
+    """Signature-id records -> class records (id field = sig_class[id])."""
+    r = np.asarray(records, np.uint32)
+    cls = np.asarray(sig_class, np.uint32)[(r >> np.uint32(1)) & np.uint32(0xFFFF)]
+    return (r & np.uint32(0xFFFE0001)) | (cls << np.uint32(1))
+
+
 class SignatureTable:
     """Interns (opcode, modifiers) signatures; the LUT holds classify()
     of each signature (ref mix.py:176-187), evaluated once per distinct
@@ -285,12 +298,15 @@ class SignatureTable:
 
 
 def pack_instructions(kernels, sigs: SignatureTable):
-    """Instruction streams -> (u32 records, u64 CSR offsets)."""
+    """Instruction streams -> (u32 class records, u64 CSR offsets): the id
+    field holds classify() of the instruction's signature (interned, so
+    classify() runs once per distinct signature); reduce with CLASS_LUT."""
     recs: list[int] = []
     offs = [0]
+    classes = sigs.classes
     for instrs in kernels:
         for ins in instrs:
-            sid = sigs.intern(ins.opcode, ins.modifiers)
+            sid = classes[sigs.intern(ins.opcode, ins.modifiers)]
             nreg = register_operand_count(ins)
             if nreg > 255:
                 raise DeviceError("instruction with more than 255 register operands")
@@ -323,8 +339,8 @@ def aggregate_batch(kernels, table: dict[str, OpClass] = DEFAULT_OPCLASSES) -> l
         return []
     sigs = SignatureTable(table)
     rec, off = pack_instructions(kernels, sigs)
-    lut = sigs.lut()
-    d_out = mix_reduce(_to_device(rec), _to_device(off), len(kernels), _to_device(lut), len(lut))
+    d_out = mix_reduce(_to_device(rec), _to_device(off), len(kernels), _to_device(CLASS_LUT),
+                       len(CLASS_LUT))
     out = _to_host(d_out, _lib.MIX, len(kernels))
     return [mix_from_record(m) for m in out]
 
@@ -598,7 +614,7 @@ class ScorePlan:
                                                           ws.ref()), "workspace")
         self.ws_bytes = ws.value
         # per-CTA partial tables K2 leaves in the workspace (score_partials)
-        self.grid_lists = self.ws_bytes // (self.n_seg * k * 8)
+        self.grid_lists = _lib.load().occx_score_lists(self._ctx)
         n_cell = self.n_var * self.n_arch
         parts = [len(blob), self.n_var * _lib.MIXSUM.itemsize, n_cell * _lib.FEAT.itemsize,
                  n_cell * _lib.VENT.itemsize, self.ws_bytes]
@@ -612,6 +628,9 @@ class ScorePlan:
         self.d_desc, self.d_pool, self.d_masks, self.d_var_kernel, d_mix = (
             _DevPtr(base + o) for o in offsets)
         self.d_sum, self.d_feat, self.d_vtab, self.d_ws = (_DevPtr(base + o) for o in offs[1:])
+        # the workspace's scheduler block starts zeroed (the scorer leaves it zero)
+        tables = self.grid_lists * self.n_seg * k * 8
+        self._d_buf[offs[4] + tables:offs[4] + self.ws_bytes].zero_()
         # K1 on device, then the feature table
         cols = [int(a["cost_key"]) for a in self.h_archs]
         feature_records(d_mix, self.n_var, cols, table.cpi_matrix(), scale,

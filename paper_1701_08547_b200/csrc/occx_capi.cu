@@ -31,7 +31,9 @@ extern "C" int occx_ctx_create(int device, occx_ctx** out) {
 extern "C" int occx_ctx_create_ex(int device, uint32_t options, occx_ctx** out) {
   if (!out) return OCCX_ERR_VALUE;
   *out = nullptr;
-  if (options & ~(uint32_t)(OCCX_CTX_K2_FEED_LDG | OCCX_CTX_K2_ONE_SLICE)) return OCCX_ERR_VALUE;
+  if (options & ~(uint32_t)(OCCX_CTX_K2_FEED_LDG | OCCX_CTX_K2_ONE_SLICE |
+                            OCCX_CTX_K2_NO_STEAL))
+    return OCCX_ERR_VALUE;
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) return OCCX_ERR_CUDA;
   cudaDeviceProp prop;

@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kMixThreads, 1) mix_reduce_kernel(const __grid
   for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) {
     uint32_t w4 = 0;
     if (4 * i < p.n_sig) {
-      if (lut_vec) {
+      if (lut_vec && 4 * i + 4 <= p.n_sig) {             // whole word inside the table
         w4 = __ldg(reinterpret_cast<const uint32_t*>(p.sig_class) + i);
       } else {
 #pragma unroll

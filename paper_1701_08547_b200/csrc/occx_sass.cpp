@@ -20,6 +20,7 @@
 #include <string>
 #include <unordered_map>
 #include <functional>
+#include <algorithm>
 #include <thread>
 #include <vector>
 
@@ -610,4 +611,32 @@ extern "C" const char* occx_sass_signature(const occx_sass* r, uint32_t i) {
   return r && i < r->sigs.size() ? r->sigs[i].c_str() : nullptr;
 }
 extern "C" const char* occx_sass_error_text(const occx_sass* r) { return r ? r->error.c_str() : ""; }
+
+// Replace every record's signature id by its class id (sig_class[sig],
+// classify() of the interned signature, mix.py:176-187): "class records",
+// reduced by K0 with the identity class table (n_sig = 15), whose lookups
+// are conflict-free in shared memory.  Threaded over record ranges.
+extern "C" int occx_sass_classify(occx_sass* r, const uint8_t* sig_class, uint32_t n_sig) {
+  if (!r || !sig_class || n_sig < r->sigs.size()) return OCCX_ERR_VALUE;
+  for (uint32_t i = 0; i < (uint32_t)r->sigs.size(); ++i)
+    if (sig_class[i] > 14) return OCCX_ERR_VALUE;
+  const size_t n = r->records.size();
+  uint32_t* rec = r->records.data();
+  auto run = [&](size_t b, size_t e) {
+    for (size_t i = b; i < e; ++i) {
+      const uint32_t x = rec[i];
+      rec[i] = (x & 0xfffe0001u) | ((uint32_t)sig_class[(x >> 1) & 0xffffu] << 1);
+    }
+  };
+  unsigned hw = std::thread::hardware_concurrency();
+  const size_t nt = std::min<size_t>(hw ? (hw < 32 ? hw : 32) : 1, n / (1u << 20) + 1);
+  if (nt <= 1) {
+    run(0, n);
+  } else {
+    std::vector<std::thread> th;
+    for (size_t t = 0; t < nt; ++t) th.emplace_back(run, n * t / nt, n * (t + 1) / nt);
+    for (auto& t : th) t.join();
+  }
+  return OCCX_OK;
+}
 extern "C" void occx_sass_free(occx_sass* r) { delete r; }

@@ -92,8 +92,10 @@ struct ScoreParams {
   uint64_t index_base;
   const occx_vent_t* vtab;
   uint32_t n_var, n_seg, k, vt_smem;
-  uint64_t chunk;           // candidates per CTA, multiple of the tile
+  uint64_t chunk;           // candidates per CTA, multiple of the tile (static feeds)
   uint64_t* partials;       // [gridDim.x][n_seg][k]
+  uint32_t* sched;          // TMA feed: taken[gridDim.x], CTAs done; zero on entry and exit
+  uint32_t steal;           // TMA feed: idle CTAs take tiles of the busiest chunk
 };
 
 // Descending bitonic sort of one u64 per lane across the warp (lane 0 = largest).
@@ -618,6 +620,9 @@ struct SepBlock {            // warp-uniform description of the tabled block
   uint32_t n, ns, seg;       // block size, |SMEM|, segment
   uint32_t ts;               // shared address of TS (TR starts at the warp's table)
   FastDiv ds;                // divide by |SMEM|
+  uint32_t hi;               // the block's key bits (high word) outside the warps field
+  // what the tables were built for: (T, arch, REGS pool, SMEM pool, ok)
+  uint32_t kt, ka, kr, ks;
 };
 
 __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
@@ -672,6 +677,12 @@ __device__ __forceinline__ uint32_t block_aw_max(const SpaceParams& q, const uin
   return bb.aw;
 }
 
+// The tables hold only the active-warps field (aw << 22; 0 when the launch
+// is illegal): they depend on (T, arch, REGS values, SMEM values) and not on
+// BC / UIF / PL / CFLAGS, so consecutive blocks of a segment (the last
+// five dimensions before REGS, SMEM vary fastest) reuse them and only the
+// block's key bits (sb.hi: legal | rule | static | rank) change.  A key's
+// high word is sb.hi | min(TR[r], TS[s]) | index bits, exactly k2_key's.
 template <int MODE, bool VT_SMEM>
 __device__ __forceinline__ bool sep_build(const SpaceParams& q, const K2Shared& s,
                                           const uint32_t* pool, const IgCache& ic,
@@ -682,29 +693,38 @@ __device__ __forceinline__ bool sep_build(const SpaceParams& q, const K2Shared& 
   const uint4 r0 = make_uint4(ic.x, 0u, ic.z, ic.w_hi);       // R, S irrelevant here
   k2_fill<VT_SMEM>(s.c, r0, kc);
   const uint32_t a = min((ic.w_hi >> 16) & 0xffu, (uint32_t)q.sp.archs.n - 1);
-  const occx_arch_t& arch = q.sp.archs.a[a];
-  const uint32_t lw = min(kc.lw, 255u), wpb = kc.wpb, wmp = kc.wmp;
-  const uint32_t hi = kc.key_hi;
-  const bool ok = kc.ok && wpb != 0;
-  __syncwarp();                                               // previous block's readers
-  for (uint32_t i = (uint32_t)lane; i < nr; i += 32) {
-    const uint32_t R = min(pool[ic.r_off + i], 0xffffu);     // record clamp (ig_record)
-    const uint32_t aw = min(min(lw, sep_lr<MODE>(arch, max(wpb, 1u), R)) * wpb, wmp);
-    sts_u32(tr + 4u * i, ok ? (hi | (aw << 22)) : 0u);
+  const bool ok = kc.ok && kc.wpb != 0;
+  const uint32_t T = ic.z & 0xffffu;
+  const uint32_t kt = T | (ok ? 0x80000000u : 0u);
+  if (sb.kt != kt || sb.ka != a || sb.kr != (ic.r_off | (nr << 20)) || sb.ks != ic.s_off ||
+      sb.ns != ns) {
+    const occx_arch_t& arch = q.sp.archs.a[a];
+    const uint32_t lw = min(kc.lw, 255u), wpb = kc.wpb, wmp = kc.wmp;
+    __syncwarp();                                             // previous block's readers
+    for (uint32_t i = (uint32_t)lane; i < nr; i += 32) {
+      const uint32_t R = min(pool[ic.r_off + i], 0xffffu);   // record clamp (ig_record)
+      const uint32_t aw = min(min(lw, sep_lr<MODE>(arch, max(wpb, 1u), R)) * wpb, wmp);
+      sts_u32(tr + 4u * i, ok ? (aw << 22) : 0u);
+    }
+    if (lane == 0) sts_u32(tr + 4u * nr, 0u);
+    for (uint32_t i = (uint32_t)lane; i < ns + 15; i += 32) {
+      const uint32_t S = pool[ic.s_off + i % ns];
+      const uint32_t aw = min(sep_ls<MODE>(arch, S) * wpb, wmp);
+      sts_u32(tr + 4u * (nr + 1 + i), ok ? (aw << 22) : 0u);
+    }
+    __syncwarp();
+    sb.kt = kt;
+    sb.ka = a;
+    sb.kr = ic.r_off | (nr << 20);
+    sb.ks = ic.s_off;
   }
-  if (lane == 0) sts_u32(tr + 4u * nr, 0u);
-  for (uint32_t i = (uint32_t)lane; i < ns + 15; i += 32) {
-    const uint32_t S = pool[ic.s_off + i % ns];
-    const uint32_t aw = min(sep_ls<MODE>(arch, S) * wpb, wmp);
-    sts_u32(tr + 4u * (nr + 1 + i), ok ? (hi | (aw << 22)) : 0u);
-  }
-  __syncwarp();
   sb.lo = ic.blk_lo;
   sb.n = ic.blk_n;
   sb.ns = ns;
   sb.seg = kc.seg;
   sb.ts = tr + 4u * (nr + 1);
   sb.ds = ic.ds;
+  sb.hi = kc.key_hi;
   return true;
 }
 
@@ -739,6 +759,8 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
   SepBlock sb;
   sb.lo = 0;
   sb.n = 0;
+  sb.ns = 0;
+  sb.kt = sb.ka = sb.kr = sb.ks = 0xffffffffu;          // no tables yet
   BlockBound bbnd;
   bbnd.z = 0xffffffffu;
   bbnd.w = bbnd.r_off = bbnd.s_off = bbnd.aw = 0;
@@ -773,7 +795,7 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
     // this conservative); wl_offer compares exactly.
     const uint64_t inv0 = kIdxMask - q.key_off - (sb_base + 4u * (uint32_t)lane);
     const uint32_t m = max(max(v[0], v[1]), max(v[2], v[3]));
-    const uint32_t mh = m | (uint32_t)(inv0 >> 32);
+    const uint32_t mh = m | sb.hi | (uint32_t)(inv0 >> 32);
     const bool any = (m & 0x1fc00000u) && mh >= (uint32_t)(s.thr[sb.seg] >> 32) &&
                      (sb.seg != wl.seg || mh > (uint32_t)(wl.thr >> 32));
     if (__any_sync(0xffffffffu, any)) {
@@ -781,7 +803,7 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
       for (int j = 0; j < 4; ++j) {
         const uint64_t inv = inv0 - (uint64_t)j;
         const uint64_t key = (v[j] & 0x1fc00000u)
-            ? (((uint64_t)(v[j] | (uint32_t)(inv >> 32)) << 32) | (uint32_t)inv) : 0ull;
+            ? (((uint64_t)(v[j] | sb.hi | (uint32_t)(inv >> 32)) << 32) | (uint32_t)inv) : 0ull;
         wl_offer(key, key ? sb.seg : wl.seg, wl, lane, p.k, s.thr, s.list, s.lock);
       }
     }
@@ -814,7 +836,7 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
     const uint64_t inv0 = kIdxMask - q.key_off - (pb + 8u * (uint32_t)lane);
     const uint32_t m = max(max(max(v[0], v[1]), max(v[2], v[3])),
                            max(max(v[4], v[5]), max(v[6], v[7])));
-    const uint32_t mh = m | (uint32_t)(inv0 >> 32);
+    const uint32_t mh = m | sb.hi | (uint32_t)(inv0 >> 32);
     const bool any = (m & 0x1fc00000u) && mh >= (uint32_t)(s.thr[sb.seg] >> 32) &&
                      (sb.seg != wl.seg || mh > (uint32_t)(wl.thr >> 32));
     if (__any_sync(0xffffffffu, any)) {
@@ -822,7 +844,7 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
       for (int j = 0; j < 8; ++j) {
         const uint64_t inv = inv0 - (uint64_t)j;
         const uint64_t key = (v[j] & 0x1fc00000u)
-            ? (((uint64_t)(v[j] | (uint32_t)(inv >> 32)) << 32) | (uint32_t)inv) : 0ull;
+            ? (((uint64_t)(v[j] | sb.hi | (uint32_t)(inv >> 32)) << 32) | (uint32_t)inv) : 0ull;
         wl_offer(key, key ? sb.seg : wl.seg, wl, lane, p.k, s.thr, s.list, s.lock);
       }
     }
@@ -847,7 +869,7 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
     uint32_t m = v[0];
 #pragma unroll
     for (int j = 1; j < 16; ++j) m = max(m, v[j]);
-    const uint32_t mh = m | (uint32_t)(inv0 >> 32);
+    const uint32_t mh = m | sb.hi | (uint32_t)(inv0 >> 32);
     const bool any = (m & 0x1fc00000u) && mh >= (uint32_t)(s.thr[sb.seg] >> 32) &&
                      (sb.seg != wl.seg || mh > (uint32_t)(wl.thr >> 32));
     if (__any_sync(0xffffffffu, any)) {
@@ -855,7 +877,7 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
       for (int j = 0; j < 16; ++j) {
         const uint64_t inv = inv0 - (uint64_t)j;
         const uint64_t key = (v[j] & 0x1fc00000u)
-            ? (((uint64_t)(v[j] | (uint32_t)(inv >> 32)) << 32) | (uint32_t)inv) : 0ull;
+            ? (((uint64_t)(v[j] | sb.hi | (uint32_t)(inv >> 32)) << 32) | (uint32_t)inv) : 0ull;
         wl_offer(key, key ? sb.seg : wl.seg, wl, lane, p.k, s.thr, s.list, s.lock);
       }
     }
@@ -1012,6 +1034,22 @@ extern "C" int occx_debug_k2_hist(uint64_t* out, int n) {
 }
 namespace {
 #endif
+// Tile schedule: CTA c owns the contiguous chunk [c*per, (c+1)*per) of
+// 16-byte-record tiles and walks it front to back, claiming kOwnBatch tiles
+// per atomicAdd on its counter taken[c] (the next batch's atomic is issued
+// when the current one starts, so its latency hides behind the ring).  A
+// CTA whose chunk is exhausted steals kStealBatch tiles at a time from the
+// front of the chunk with the most tiles left (warp 0 scans the counters),
+// so CTAs on slower SMs no longer set the kernel's end (a static split
+// left the slowest SMs ~20 % behind the median).  Owner and thieves claim
+// through the same counter, so every tile is taken exactly once.  Fully
+// dynamic single-counter schedules were measured 1.45-2.8x slower (contended
+// atomics on the producer's critical path).  The tile index reaches the
+// consumers in the stage's tile_of slot; kTileEnd ends the CTA's work.  The
+// last CTA to finish returns the counters to zero for the next launch.
+constexpr uint32_t kTileEnd = 0xffffffffu;
+constexpr uint32_t kOwnBatch = 4, kStealBatch = 2;
+
 template <int MODE, bool VT_SMEM, int SL>
 __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __grid_constant__ ScoreParams p) {
   constexpr int kTmaSlices = SL;
@@ -1022,31 +1060,99 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
   uint4* ring = reinterpret_cast<uint4*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTmaRingBytes);
   uint64_t* empty = full + kTmaStages;
+  volatile uint32_t* tile_of = reinterpret_cast<volatile uint32_t*>(empty + kTmaStages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t begin = (uint64_t)blockIdx.x * p.chunk;
-  const uint64_t end = begin + p.chunk < p.n ? begin + p.chunk : p.n;
-  const uint32_t n_tiles = begin < end ? (uint32_t)((end - begin + kTmaTile - 1) / kTmaTile) : 0u;
-  const uint32_t first = n_tiles < (uint32_t)kTmaStages ? n_tiles : (uint32_t)kTmaStages;
+  const uint32_t n_tiles = (uint32_t)((p.n + kTmaTile - 1) / kTmaTile);
   uint64_t policy = 0;
+  // producer state (warp 0, warp-uniform; lane 0 issues)
+  uint32_t issued = 0, next = 0;
+  bool ended = false;
+  const uint32_t G = gridDim.x, c = blockIdx.x;
+  const uint32_t per = (n_tiles + G - 1) / G;
+  auto chunk_len = [&](uint32_t v) -> uint32_t {
+    const uint64_t lo = (uint64_t)v * per;
+    return lo < n_tiles ? (uint32_t)min((uint64_t)per, n_tiles - lo) : 0u;
+  };
+  const uint32_t own_len = chunk_len(c);
+  uint32_t cur = 0, cur_hi = 0, pre = 0;       // current claimed range; prefetched claim
+  bool own_done = own_len == 0, steal_done = p.steal == 0;
+  if (warp == 0 && lane == 0 && !own_done) pre = atomicAdd(p.sched + c, kOwnBatch);
+  // next tile of this CTA (warp 0, all lanes), n_tiles at the end
+  auto grab = [&]() -> uint32_t {
+    if (cur < cur_hi) return cur++;
+    if (!own_done) {
+      const uint32_t t0 = __shfl_sync(0xffffffffu, pre, 0);
+      if (t0 < own_len) {
+        cur = c * per + t0;
+        cur_hi = c * per + min(t0 + kOwnBatch, own_len);
+        if (lane == 0) pre = atomicAdd(p.sched + c, kOwnBatch);
+        return cur++;
+      }
+      own_done = true;
+    }
+    while (!steal_done) {
+      // the chunk with the most unclaimed tiles (ties: lowest index)
+      uint64_t best = 0;
+      for (uint32_t v = (uint32_t)lane; v < G; v += 32) {
+        const uint32_t tk = *(volatile uint32_t*)(p.sched + v), len = chunk_len(v);
+        if (tk < len) best = max(best, ((uint64_t)(len - tk) << 32) | (0xffffffffu - v));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+      if (best == 0) break;
+      const uint32_t v = 0xffffffffu - (uint32_t)best;
+      uint32_t t0 = 0;
+      if (lane == 0) t0 = atomicAdd(p.sched + v, kStealBatch);
+      t0 = __shfl_sync(0xffffffffu, t0, 0);
+      const uint32_t len = chunk_len(v);
+      if (t0 < len) {
+        cur = v * per + t0;
+        cur_hi = v * per + min(t0 + kStealBatch, len);
+        return cur++;
+      }
+    }
+    steal_done = true;
+    return n_tiles;
+  };
 #ifdef OCCX_K2_TIMING
   if (threadIdx.x == 0) g_k2_timing[blockIdx.x * 8 + 0] = k2_gt();
 #endif
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kTmaStages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kTmaConsumerWarps);
+  // issue tile `tile` into stage st (or the end marker)
+  auto issue = [&](uint32_t st, uint32_t tile) {     // warp 0; lane 0 issues
+    if (tile >= n_tiles) {
+      if (lane == 0) {
+        tile_of[st] = kTileEnd;
+        mbar_arrive(&full[st]);
+      }
+      ended = true;
+      return;
     }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    if (lane == 0) {
+      tile_of[st] = tile;
+      const uint64_t tb = (uint64_t)tile * kTmaTile;
+      const uint32_t cnt = (uint32_t)min((uint64_t)kTmaTile, p.n - tb);
+      mbar_expect_tx(&full[st], cnt * 16u);
+      tma_load_1d(ring + (size_t)st * kTmaTile, p.cand + tb, cnt * 16u, &full[st], policy);
+    }
+  };
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < kTmaStages; ++i) {
+        mbar_init(&full[i], 1);
+        mbar_init(&empty[i], kTmaConsumerWarps);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    }
+    __syncwarp();
     // the first ring round needs no free slot: start it before the table setup
-    for (uint32_t t = 0; t < first; ++t) {
-      const uint64_t tb = begin + (uint64_t)t * kTmaTile;
-      const uint32_t cnt = (uint32_t)min((uint64_t)kTmaTile, end - tb);
-      mbar_expect_tx(&full[t], cnt * 16u);
-      tma_load_1d(ring + (size_t)t * kTmaTile, p.cand + tb, cnt * 16u, &full[t], policy);
+    next = grab();
+    while (issued < (uint32_t)kTmaStages && !ended) {
+      issue(issued++, next);
+      if (!ended) next = grab();
     }
   }
-  const K2Shared s = k2_setup<MODE, VT_SMEM>(p, smem + kTmaRingBytes + 2 * kTmaStages * 8);
+  const K2Shared s = k2_setup<MODE, VT_SMEM>(p, smem + kTmaRingBytes + 2 * kTmaStages * 8 + 16);
   uint64_t* stage = reinterpret_cast<uint64_t*>(const_cast<int*>(s.lock + p.n_seg)) + 1;
   stage = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(stage) + 7) & ~uintptr_t(7));
   __syncthreads();
@@ -1056,29 +1162,26 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
     g_k2_timing[blockIdx.x * 8 + 1] = k2_gt();
     g_k2_timing[blockIdx.x * 8 + 4] = sm;
-    g_k2_timing[blockIdx.x * 8 + 5] = n_tiles;
   }
 #endif
   if (warp == 0) {
-    if (lane == 0) {
-      for (uint32_t t = first; t < n_tiles; ++t) {
-        const uint32_t st = t % kTmaStages;
-        mbar_wait(&empty[st], ((t / kTmaStages) & 1u) ^ 1u);
-        const uint64_t tb = begin + (uint64_t)t * kTmaTile;
-        const uint32_t cnt = (uint32_t)min((uint64_t)kTmaTile, end - tb);
-        mbar_expect_tx(&full[st], cnt * 16u);
-        tma_load_1d(ring + (size_t)st * kTmaTile, p.cand + tb, cnt * 16u, &full[st], policy);
-      }
+    for (uint32_t t = issued; !ended; ++t) {
+      const uint32_t st = t % kTmaStages;
+      mbar_wait(&empty[st], ((t / kTmaStages) & 1u) ^ 1u);
+      issue(st, next);
+      if (!ended) next = grab();
+      issued = t + 1;
     }
+#ifdef OCCX_K2_TIMING
+    if (lane == 0) g_k2_timing[blockIdx.x * 8 + 5] = issued - 1;
+#endif
   } else {
     WarpList wl{0, 0, kNoSeg, kNoSeg, 0};
     K2Cache cc;
     cc.x = cc.z = cc.w = 0xffffffffu;
     k2_fill<VT_SMEM>(s.c, make_uint4(0xffffffffu, 0, 0, 0xffffffffu), cc);
-    for (uint32_t t = 0; t < n_tiles; ++t) {
+    for (uint32_t t = 0;; ++t) {
       const uint32_t st = t % kTmaStages;
-      const uint64_t tb = begin + (uint64_t)t * kTmaTile;
-      const uint32_t cnt = (uint32_t)min((uint64_t)kTmaTile, end - tb);
 #ifdef OCCX_K2_TIMING
       const long long w0 = k2_clk();
 #endif
@@ -1086,7 +1189,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
 #ifdef OCCX_K2_TIMING
       K2_ADD(7, k2_clk() - w0);
 #endif
-      const uint4* tile = ring + (size_t)st * kTmaTile;
+      const uint32_t tile = tile_of[st];
+      if (tile == kTileEnd) break;
+      const uint64_t tb = (uint64_t)tile * kTmaTile;
+      const uint32_t cnt = (uint32_t)min((uint64_t)kTmaTile, p.n - tb);
+      const uint4* ring_tile = ring + (size_t)st * kTmaTile;
       // warp w takes kTmaSlices contiguous 128-record slices of the tile, so
       // its (T, variant, arch) cache sees kTmaSlices x 128 consecutive records
       const uint32_t slice = (uint32_t)(warp - 1) * (128u * kTmaSlices) + lane;
@@ -1095,14 +1202,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
 #pragma unroll
         for (int h = 0; h < kTmaSlices; ++h)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) r[h][j] = tile[slice + 128u * h + 32u * j];
+          for (int j = 0; j < 4; ++j) r[h][j] = ring_tile[slice + 128u * h + 32u * j];
       } else {
 #pragma unroll
         for (int h = 0; h < kTmaSlices; ++h)
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const uint32_t idx = slice + 128u * h + 32u * j;
-            r[h][j] = idx < cnt ? tile[idx] : make_uint4(0, 0, 0, 0xffffffffu);
+            r[h][j] = idx < cnt ? ring_tile[idx] : make_uint4(0, 0, 0, 0xffffffffu);
           }
       }
       __syncwarp();
@@ -1116,7 +1223,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
                                    lane, p.k);
 #ifdef OCCX_K2_TIMING
       if (lane == 0)
-        atomicAdd(&g_k2_hist[blockIdx.x * 16 + (t * 16u) / n_tiles], (unsigned long long)(k2_clk() - p0));
+        atomicAdd(&g_k2_hist[blockIdx.x * 16 + (tile * 16u) / n_tiles], (unsigned long long)(k2_clk() - p0));
 #endif
     }
     k2_stage(wl, lane, p.k, stage, warp - 1, kTmaConsumerWarps);
@@ -1128,6 +1235,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
   if (warp == 1) k2_merge_staged(stage, 2 * kTmaConsumerWarps, p.k, s.thr, s.list, s.lock);
   __syncthreads();
   k2_flush(p, s);
+  if (threadIdx.x == 0) {
+    // every producer of the grid has finished taking tiles once all CTAs
+    // have counted themselves here: the last one resets the scheduler
+    if (atomicAdd(p.sched + gridDim.x, 1u) == gridDim.x - 1)
+      for (uint32_t v = 0; v <= gridDim.x; ++v) p.sched[v] = 0;
+  }
 #ifdef OCCX_K2_TIMING
   __syncthreads();
   if (threadIdx.x == 0) g_k2_timing[blockIdx.x * 8 + 3] = k2_gt();
@@ -1449,12 +1562,21 @@ static int score_grid(const occx_ctx* ctx) {
   return score_feed(ctx) == kFeedTma ? ctx->sm_count : ctx->sm_count * 2;
 }
 
+// Workspace: [score_grid][n_seg][k] per-CTA tables, then a 256-byte
+// scheduler block (TMA feed tile counter); zero before the first call,
+// every call leaves it zero.
+static uint64_t sched_bytes(const occx_ctx* ctx) {      // taken[grid] + done, 256-B units
+  return ((uint64_t)(score_grid(ctx) + 1) * 4 + 255) / 256 * 256;
+}
+
 extern "C" int occx_score_workspace_bytes(const occx_ctx* ctx, uint32_t n_seg, uint32_t k,
                                           uint64_t* bytes) {
   if (!ctx || !bytes || k == 0 || k > OCCX_MAX_K || n_seg == 0) return OCCX_ERR_VALUE;
-  *bytes = (uint64_t)score_grid(ctx) * n_seg * k * 8;
+  *bytes = (uint64_t)score_grid(ctx) * n_seg * k * 8 + sched_bytes(ctx);
   return OCCX_OK;
 }
+
+extern "C" int occx_score_lists(const occx_ctx* ctx) { return ctx ? score_grid(ctx) : 0; }
 
 extern "C" int occx_topk_merge(const occx_ctx* ctx, const uint64_t* d_lists, uint32_t n_lists,
                                uint32_t n_seg, uint32_t k, uint64_t* d_out, void* stream) {
@@ -1492,6 +1614,8 @@ extern "C" int occx_score_topk(const occx_ctx* ctx, const occx_arch_t* h_archs, 
   p.partials = static_cast<uint64_t*>(d_ws);
   const int grid = score_grid(ctx);
   const int feed = score_feed(ctx);
+  p.sched = reinterpret_cast<uint32_t*>(static_cast<char*>(d_ws) + need - sched_bytes(ctx));
+  p.steal = (ctx->options & OCCX_CTX_K2_NO_STEAL) ? 0u : 1u;
   p.vt_smem = ((uint64_t)n_var * n_arch <= (uint64_t)kVtSmemMax) ? 1u : 0u;
   size_t smem = k2_tail_bytes(p.archs, n_var, n_seg, k, p.vt_smem != 0);
   // two slices per warp (64 KB stages, 192 KB in flight per SM) whenever the
@@ -1500,11 +1624,11 @@ extern "C" int occx_score_topk(const occx_ctx* ctx, const occx_arch_t* h_archs, 
   // (context option) forces one.
   const bool one_slice = (ctx->options & OCCX_CTX_K2_ONE_SLICE) != 0;
   int sl = (feed == kFeedTma && !one_slice &&
-            smem + TmaRing<2>::kBytes + 2 * TmaRing<2>::kStages * 8 <= (size_t)ctx->max_smem_optin)
+            smem + TmaRing<2>::kBytes + 2 * TmaRing<2>::kStages * 8 + 16 <= (size_t)ctx->max_smem_optin)
                ? 2 : 1;
   if (feed == kFeedTma)
-    smem += sl == 2 ? TmaRing<2>::kBytes + 2 * TmaRing<2>::kStages * 8
-                    : TmaRing<1>::kBytes + 2 * TmaRing<1>::kStages * 8;
+    smem += (sl == 2 ? TmaRing<2>::kBytes + 2 * TmaRing<2>::kStages * 8
+                     : TmaRing<1>::kBytes + 2 * TmaRing<1>::kStages * 8) + 16;   // + tile_of
   const uint64_t tile = feed == kFeedTma ? (uint64_t)kTmaTile * sl : (uint64_t)kLdgThreads * kLdgUnroll;
   const uint64_t tiles = (n + tile - 1) / tile;
   p.chunk = ((tiles + grid - 1) / grid) * tile;

@@ -36,7 +36,7 @@ from . import __version__, _lib
 from .arch import ArchSpec
 from .batch import (FeatureBatch, SignatureTable, _to_device, _to_host, cost_key_of_cc,
                     feature_records, mix_from_record, mix_reduce, occupancy_batch,
-                    pack_instructions, suggest_batch)
+                    pack_instructions, suggest_batch, CLASS_LUT)
 from .mix import (DEFAULT_OPCLASSES, DEFAULT_THROUGHPUT, InstructionMix, OpClass,
                   category_cycles, per_class_cycles, pipeline_utilization)
 from .occupancy import Mode, OccupancyResult, SuggestionReport
@@ -136,7 +136,7 @@ def analyze_batch(arch: ArchSpec, items, mode: Mode = Mode.CORRECTED,
     rec, off = pack_instructions([ins for _, ins in items], sigs)
     return _pipeline(arch, [r for r, _ in items], _to_device(rec if len(rec) else
                                                              np.zeros(1, np.uint32)),
-                     _to_device(off), len(items), sigs.lut(), list(range(len(items))), mode,
+                     _to_device(off), len(items), CLASS_LUT, list(range(len(items))), mode,
                      dynamic_shared_mem, space if space is not None else TuningSpace(), scale)
 
 
@@ -159,7 +159,8 @@ def analyze_listing(arch: ArchSpec, resource_report: str, disassembly: str,
     as the reference's dict does), or an empty stream with a warning."""
     from .sass import tokenize
     resources = parse_resource_report(resource_report)
-    toks = tokenize(disassembly)
+    toks = tokenize(disassembly, table=opclass_table if opclass_table is not None
+                    else DEFAULT_OPCLASSES)
     by_name = {name: k for k, name in enumerate(toks.names)}
     n_k = len(toks.names)
     kernel_of = []
@@ -172,9 +173,8 @@ def analyze_listing(arch: ArchSpec, resource_report: str, disassembly: str,
             k = n_k                                  # the shared empty stream
         kernel_of.append(k)
     off = np.concatenate([toks.offsets, toks.offsets[-1:]]).astype(np.uint64)
-    lut = toks.class_lut(opclass_table if opclass_table is not None else DEFAULT_OPCLASSES)
     rec = toks.records if len(toks.records) else np.zeros(1, np.uint32)
-    return _pipeline(arch, resources, _to_device(rec), _to_device(off), n_k + 1, lut,
+    return _pipeline(arch, resources, _to_device(rec), _to_device(off), n_k + 1, CLASS_LUT,
                      kernel_of, mode, dynamic_shared_mem,
                      space if space is not None else TuningSpace(), scale)
 

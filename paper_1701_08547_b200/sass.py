@@ -35,9 +35,13 @@ class SassRecords:
         return np.asarray(lut or [DEVICE_ID[OpClass.UNCLASSIFIED]], np.uint8)
 
 
-def tokenize(text: str, chunk_bytes: int = 0) -> SassRecords:
+def tokenize(text: str, chunk_bytes: int = 0, table=None) -> SassRecords:
     """``chunk_bytes``: minimum bytes per worker-thread chunk (0 = library
-    default); only the split changes, never the result."""
+    default); only the split changes, never the result.  ``table`` (an
+    opcode-class table): emit class records -- each record's signature id
+    replaced by classify() of its signature (occx_sass_classify), for K0 with
+    the identity class table ``CLASS_LUT``; ``signatures`` still lists the
+    interned signatures."""
     lib = _lib.load()
     data = text.encode("utf-8", "surrogatepass")
     h = ctypes.c_void_p()
@@ -63,14 +67,18 @@ def tokenize(text: str, chunk_bytes: int = 0) -> SassRecords:
         off = np.ctypeslib.as_array(ctypes.cast(lib.occx_sass_offsets(h),
                                                 ctypes.POINTER(ctypes.c_uint64)),
                                     shape=(n_k + 1,)).copy() if n_k else np.zeros(1, np.uint64)
-        rec = np.ctypeslib.as_array(ctypes.cast(lib.occx_sass_records(h),
-                                                ctypes.POINTER(ctypes.c_uint32)),
-                                    shape=(n_i,)).copy() if n_i else np.zeros(0, np.uint32)
         sigs = []
         for i in range(lib.occx_sass_n_sigs(h)):
             parts = lib.occx_sass_signature(h, i).decode("utf-8", "surrogatepass").split("\x1f")
             sigs.append((parts[0], tuple("." + m for m in parts[1:])))
-        return SassRecords(names, off, rec, sigs)
+        out = SassRecords(names, off, None, sigs)
+        if table is not None and n_i:
+            lut = out.class_lut(table)
+            _lib.check(lib.occx_sass_classify(h, lut.ctypes.data, len(lut)), "occx_sass_classify")
+        out.records = np.ctypeslib.as_array(
+            ctypes.cast(lib.occx_sass_records(h), ctypes.POINTER(ctypes.c_uint32)),
+            shape=(n_i,)).copy() if n_i else np.zeros(0, np.uint32)
+        return out
     finally:
         lib.occx_sass_free(h)
 
@@ -78,12 +86,11 @@ def tokenize(text: str, chunk_bytes: int = 0) -> SassRecords:
 def aggregate_text(text: str, table=DEFAULT_OPCLASSES) -> list:
     """[(name, InstructionMix)] for every function of a listing: native
     tokenizer + K0 on the GPU."""
-    from .batch import _to_device, _to_host, mix_from_record, mix_reduce
-    r = tokenize(text)
+    from .batch import CLASS_LUT, _to_device, _to_host, mix_from_record, mix_reduce
+    r = tokenize(text, table=table)
     if not r.names:
         return []
-    lut = r.class_lut(table)
     d = mix_reduce(_to_device(r.records if len(r.records) else np.zeros(1, np.uint32)),
-                   _to_device(r.offsets), len(r.names), _to_device(lut), len(lut))
+                   _to_device(r.offsets), len(r.names), _to_device(CLASS_LUT), len(CLASS_LUT))
     out = _to_host(d, _lib.MIX, len(r.names))
     return [(n, mix_from_record(m)) for n, m in zip(r.names, out)]

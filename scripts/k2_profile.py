@@ -28,10 +28,15 @@ timing = hasattr(lib, "occx_debug_k2_timing") and "timing" in (os.environ.get("O
 
 
 def timed(fn, reps=15, do_flush=True):
+    """GPU time of one launch.  The start event is queued behind a busy
+    kernel (the L2 flush, or a 200 us spin when the input is far above L2),
+    so the host's launch overhead is not inside the events."""
     ts = []
     for _ in range(reps):
         if do_flush:
             flush.fill_(1)
+        else:
+            torch.cuda._sleep(400_000)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         fn()
@@ -54,7 +59,8 @@ def main():
     names = sys.argv[1:] or ["config2", "config4", "shard8", "config5"]
     for name in names:
         cfg, begin, n = workload(name)
-        plan = ScorePlan(cfg.kernels, cfg.archs, "corrected", k=cfg.k)
+        plan = ScorePlan(cfg.kernels, cfg.archs, "corrected", k=cfg.k,
+                         options=int(os.environ.get("K2_OPTIONS", "0"), 0))
         n = plan.total if n is None else n
         rec = plan.generate(begin, n)
         out = torch.empty((plan.n_seg, plan.k), dtype=torch.int64, device="cuda")

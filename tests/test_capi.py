@@ -36,7 +36,7 @@ def test_abi_version_and_status_strings(lib):
 
 def test_ctx_options_validated_before_device(lib):
     out = ctypes.c_void_p()
-    assert lib.occx_ctx_create_ex(0, 0x4, ctypes.byref(out)) == 1       # unknown option bit
+    assert lib.occx_ctx_create_ex(0, 0x10, ctypes.byref(out)) == 1      # unknown option bit
     assert lib.occx_ctx_create_ex(0, 0, None) == 1
     assert lib.occx_ctx_options(None) == 0
 

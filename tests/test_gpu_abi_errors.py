@@ -96,10 +96,11 @@ def test_score_space_flags_checked(env):
     assert call(0x2) == 1                                 # unknown flag bit: ValueError
 
 
-@pytest.mark.parametrize("options", [1, 2, 3])
+@pytest.mark.parametrize("options", [1, 2, 3, 4, 6])
 def test_ctx_options_same_topk(env, options):
     """The LDG-fed K2 (two 512-thread CTAs per SM, doubled workspace) and the
-    one-slice TMA ring give the default's top-k on config 2 (golden)."""
+    one-slice TMA ring and the dynamic tile schedules give the default's top-k
+    on config 2 (golden)."""
     from helpers import load_golden
     from paper_1701_08547_b200 import ScorePlan, workloads
     torch, L, lib, _, _ = env
