@@ -857,7 +857,7 @@ def main():
                     segs, keys = api_step(prune)
                 e1.record(stream)
                 torch.cuda.synchronize()
-                assert np.array_equal(keys.numpy().view(np.uint64), final_keys), \
+                assert np.array_equal(np.asarray(keys).view(np.uint64).reshape(final_keys.shape), final_keys), \
                     "API top-k differs from the record path"
                 return max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
             # headline: every candidate's key evaluated (block pruning off)

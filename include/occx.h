@@ -289,6 +289,30 @@ int occx_score_space(const occx_ctx* ctx, const occx_arch_t* h_archs, int n_arch
                      uint32_t n_seg, uint32_t k, void* d_ws, uint64_t ws_bytes,
                      uint64_t* d_topk, void* stream);
 
+/* ---- score_space() in one call ----------------------------------------
+ * The whole public score_space() step on `stream`: copy the packed space
+ * description h_blob (blob_off[5] byte offsets of: occx_segdesc_t[n_seg] |
+ * u32 value pool[n_pool] | u64 membership masks[n_seg][3] (static,
+ * rule-lower, rule-upper; bit t/32-1) | u32 var_kernel[n_var] |
+ * occx_mix_t[n_var]) to d_buf, run K1 (h_cpi[4][16], scale, sum_mode) + the
+ * feature table + K2i over candidates [begin, begin+n) (keys carry index +
+ * key_offset) + K3, and copy the [n_seg][k] top-k keys to h_topk, returning
+ * when they are there.  h_topk == NULL: no copy and no wait; the table is
+ * left at d_buf + occx_space_buf_bytes' *topk_off.  Replaces the
+ * per-candidate occupancy / static_prune / rule_prune / cost_estimate loop
+ * the reference's users write (occupancy.py:163-195, tuning.py:94-127,
+ * mix.py:321-337).                                                       */
+int occx_space_buf_bytes(const occx_ctx* ctx, uint64_t blob_bytes, uint32_t n_var,
+                         uint32_t n_arch, uint32_t n_seg, uint32_t k, uint64_t* bytes,
+                         uint64_t* topk_off);
+int occx_score_space_host(const occx_ctx* ctx, const occx_arch_t* h_archs, int n_arch,
+                          const void* h_blob, uint64_t blob_bytes, const uint64_t* blob_off,
+                          uint32_t n_seg, uint32_t n_pool, uint32_t n_var,
+                          const double* h_cpi, double scale, int sum_mode,
+                          uint64_t begin, uint64_t n, uint64_t key_offset, int mode,
+                          uint32_t flags, uint32_t k, void* d_buf, uint64_t buf_bytes,
+                          uint64_t* h_topk, void* stream);
+
 /* ---- candidate generator ----------------------------------------------
  * enumerate_space() tuning.py:75-77 decoded on device: writes candidates
  * [begin, begin+n) of the concatenated segments.                       */

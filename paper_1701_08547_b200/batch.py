@@ -14,6 +14,8 @@ from liboccx.so.  Host code packs inputs, launches, and unpacks results.
 from __future__ import annotations
 
 import bisect
+import ctypes
+import functools
 import sys
 from dataclasses import dataclass, field
 from typing import Sequence
@@ -541,6 +543,80 @@ def decode_key(key: int) -> dict:
             "rank_bits": rb, "index": IDX_MASK - (key & IDX_MASK)}
 
 
+@functools.lru_cache(maxsize=64)
+def _packed_archs(archs: tuple) -> np.ndarray:
+    """occx_arch_t rows of an arch tuple: an arch-level table (like
+    thread_candidates), memoised on the frozen specs."""
+    out = pack_archs(archs)
+    out.setflags(write=False)
+    return out
+
+
+class _SpacePack:
+    """The host side of a (kernels x archs) search: the packed space
+    description (csrc/occx_host.cpp pack_plan: segment descriptors, value
+    pool, membership masks, variant -> kernel, mixes; one H2D blob) and what
+    decoding keys needs.  Segment s = kernel * n_arch + arch."""
+
+    def __init__(self, kernels, archs, k: int):
+        if not 1 <= k <= 32:
+            raise ValueError("k must be in [1, 32]")
+        self.kernels = list(kernels)
+        self.archs = list(archs)
+        self.k = k
+        self.n_arch = len(self.archs)
+        self.n_seg = len(self.kernels) * self.n_arch
+        self.h_archs = _packed_archs(tuple(self.archs))
+        mixes, self.var_base, var_counts = [], [], []
+        dims_all, self.kern_dims = [], []
+        for kern in self.kernels:
+            n_v = len(kern.mixes)
+            if n_v != kern.n_variants():
+                raise ValueError(f"{kern.name}: need one mix per (UIF, CFLAGS) variant")
+            self.var_base.append(len(mixes))
+            var_counts.append(n_v)
+            mixes += kern.mixes
+            sp = kern.space
+            regs, smem = (kern.registers_per_thread,), (kern.static_shared_mem,)
+            if sp.extra:
+                names = [n.upper() for n, _ in sp.extra]
+                if any(n not in ("REGS", "SMEM") for n in names) or names not in (
+                        ["REGS"], ["SMEM"], ["REGS", "SMEM"]):
+                    raise ValueError("extra dimensions must be REGS and/or SMEM, in that order")
+                extras = {name.upper(): vals for name, vals in sp.extra}
+                regs, smem = extras.get("REGS", regs), extras.get("SMEM", smem)
+            dims_all.append((sp.thread_counts, sp.block_counts, sp.unroll_factors,
+                             sp.l1_sizes_kb, sp.compiler_flags, regs, smem))
+            self.kern_dims.append([tuple(v) for _, v in sp._dimensions()])
+        self.mixes = mixes
+        self.n_var = len(mixes)
+        self.var_counts = var_counts
+        (self.blob, self.offsets, self.total, self.n_pool,
+         self.seg_start) = _host().pack_plan(dims_all, var_counts, mixes,
+                                             [thread_candidates(a) for a in self.archs],
+                                             DEVICE_ID, DeviceError)
+        if self.total > IDX_MASK + 1:
+            raise DeviceError("search space above 2^34 candidates")
+
+    @property
+    def seg_dims(self) -> list:
+        return [d for d in self.kern_dims for _ in range(self.n_arch)]
+
+    def decode(self, keys) -> list[SegmentTopK]:
+        """[n_seg, k] keys -> per-segment Ranked entries (native: key fields,
+        global index -> enumerate_space digits, last dimension fastest, ref
+        tuning.py:70-77).  Indices of weak-scaling copies are taken modulo
+        total."""
+        keys = np.asarray(keys.cpu().numpy() if hasattr(keys, "cpu") else keys)
+        keys = np.ascontiguousarray(keys).view(np.uint64).reshape(self.n_seg, self.k)
+        segs = _host().decode(keys, self.n_arch, self.k, self.total, self.seg_start,
+                              self.kern_dims, self.var_base)
+        names = [a.name for a in self.archs]
+        na = self.n_arch
+        return [SegmentTopK(self.kernels[s // na].name, names[s % na], e)
+                for s, e in enumerate(segs)]
+
+
 class ScorePlan:
     """Device-resident tables for scoring a fixed (kernels x archs) search.
 
@@ -559,50 +635,19 @@ class ScorePlan:
         if not 1 <= k <= 32:
             raise ValueError("k must be in [1, 32]")
         self._ctx = _lib.ctx(options=options)
-        self.kernels = list(kernels)
-        self.archs = list(archs)
+        pk = _SpacePack(kernels, archs, k)
+        self._pack = pk
+        self.kernels, self.archs, self.k = pk.kernels, pk.archs, k
         self.mode = Mode(mode)
-        self.k = k
-        self.n_arch = len(self.archs)
-        self.n_seg = len(self.kernels) * self.n_arch
-        self.h_archs = pack_archs(self.archs)
-        # variants
-        mixes, var_kernel, self.var_base = [], [], []
-        for ki, kern in enumerate(self.kernels):
-            if len(kern.mixes) != kern.n_variants():
-                raise ValueError(f"{kern.name}: need one mix per (UIF, CFLAGS) variant")
-            self.var_base.append(len(mixes))
-            mixes += list(kern.mixes)
-            var_kernel += [ki] * len(kern.mixes)
-        self.n_var = len(mixes)
-        # segments: descriptors + value pool + masks + variants + mixes,
-        # packed natively (csrc/occx_host.cpp) into one H2D blob.  The value
-        # pool of a kernel's seven dimensions is shared by its n_arch segments.
-        dims_all, self.seg_dims, self.kern_dims = [], [], []
-        for kern in self.kernels:
-            sp = kern.space
-            names = [n.upper() for n, _ in sp.extra]
-            if any(n not in ("REGS", "SMEM") for n in names) or names not in (
-                    [], ["REGS"], ["SMEM"], ["REGS", "SMEM"]):
-                raise ValueError("extra dimensions must be REGS and/or SMEM, in that order")
-            extras = {name.upper(): vals for name, vals in sp.extra}
-            dims_all.append((sp.thread_counts, sp.block_counts, sp.unroll_factors,
-                             sp.l1_sizes_kb, sp.compiler_flags,
-                             extras.get("REGS", (kern.registers_per_thread,)),
-                             extras.get("SMEM", (kern.static_shared_mem,))))
-            seg_dims = [tuple(v) for _, v in sp._dimensions()]
-            self.kern_dims.append(seg_dims)
-            self.seg_dims += [seg_dims] * self.n_arch
-        blob, offsets, self.total, self.n_pool = _host().pack_plan(
-            dims_all, [len(k.mixes) for k in self.kernels], mixes,
-            [thread_candidates(a) for a in self.archs], DEVICE_ID, DeviceError)
-        if self.total > IDX_MASK + 1:
-            raise DeviceError("search space above 2^34 candidates")
-        desc = np.frombuffer(blob, _lib.SEGDESC, self.n_seg, offsets[0])
-        self._seg_start_np = desc["start"].astype(np.int64)
-        self.seg_start = self._seg_start_np.tolist()
+        self.n_arch, self.n_seg, self.n_var = pk.n_arch, pk.n_seg, pk.n_var
+        self.h_archs = pk.h_archs
+        self.var_base, self.kern_dims, self.seg_start = pk.var_base, pk.kern_dims, pk.seg_start
+        self.total, self.n_pool, self.mixes = pk.total, pk.n_pool, pk.mixes
+        self.seg_dims = pk.seg_dims
+        blob, offsets = pk.blob, pk.offsets
+        var_kernel = [ki for ki, nv in enumerate(pk.var_counts) for _ in range(nv)]
         self.var_kernel = np.asarray(var_kernel, np.uint32)
-        self.mixes = mixes
+        self._seg_start_np = np.asarray(self.seg_start, np.int64)
         self._blob, self._offsets = blob, offsets
         # bytes this plan copied host -> device (the space description; the
         # arch rows and CPI table travel in the kernel parameter blocks)
@@ -738,13 +783,7 @@ class ScorePlan:
 
     def merge(self, d_lists, n_lists: int, out=None, stream=None):
         """K3 over [n_lists, n_seg, k] device tables -> [n_seg, k]."""
-        torch = _torch()
-        out = out if out is not None else torch.empty((self.n_seg, self.k), dtype=torch.int64,
-                                                      device="cuda")
-        _lib.check(_lib.load().occx_topk_merge(
-            self._ctx, _lib.ptr(d_lists), n_lists, self.n_seg, self.k, _lib.ptr(out),
-            _lib.stream_ptr(stream)), "occx_topk_merge")
-        return out
+        return merge_tables(d_lists, n_lists, self.n_seg, self.k, out, stream, self._ctx)
 
     # -- decoding -----------------------------------------------------------
     def locate(self, gidx: int) -> tuple[int, tuple]:
@@ -759,18 +798,18 @@ class ScorePlan:
         return s, tuple(reversed(digits))
 
     def decode(self, keys) -> list[SegmentTopK]:
-        """[n_seg, k] keys -> per-segment Ranked entries (host, native: the
-        key fields, the global index -> enumerate_space digits, last
-        dimension fastest, ref tuning.py:70-77).  Indices of weak-scaling
-        copies are taken modulo total."""
-        keys = np.asarray(keys.cpu().numpy() if hasattr(keys, "cpu") else keys)
-        keys = np.ascontiguousarray(keys).view(np.uint64).reshape(self.n_seg, self.k)
-        segs = _host().decode(keys, self.n_arch, self.k, self.total, self.seg_start,
-                              self.kern_dims, self.var_base)
-        names = [a.name for a in self.archs]
-        na = self.n_arch
-        return [SegmentTopK(self.kernels[s // na].name, names[s % na], e)
-                for s, e in enumerate(segs)]
+        """[n_seg, k] keys -> per-segment Ranked entries (_SpacePack.decode)."""
+        return _SpacePack.decode(self, keys)
+
+
+def merge_tables(d_lists, n_lists: int, n_seg: int, k: int, out=None, stream=None, ctx=None):
+    """K3: [n_lists, n_seg, k] device top-k tables -> merged [n_seg, k]."""
+    torch = _torch()
+    out = out if out is not None else torch.empty((n_seg, k), dtype=torch.int64, device="cuda")
+    _lib.check(_lib.load().occx_topk_merge(
+        ctx if ctx is not None else _lib.ctx(), _lib.ptr(d_lists), n_lists, n_seg, k,
+        _lib.ptr(out), _lib.stream_ptr(stream)), "occx_topk_merge")
+    return out
 
 
 class ctypes_u64:
@@ -795,6 +834,34 @@ def score_space(kernels: Sequence[KernelSpec], archs: Sequence[ArchSpec],
     from their index inside the scorer (K2i): nothing but the space
     description, the feature table and the top-k table touch HBM.
     ``prune=False`` evaluates every key (no exact block skipping)."""
-    plan = ScorePlan(kernels, archs, mode, k)
-    keys = plan.score_implicit(prune=prune)
-    return plan.decode(keys)
+    return space_score(_SpacePack(kernels, archs, k), mode, prune=prune)[0]
+
+
+def space_score(pk: _SpacePack, mode=Mode.CORRECTED, begin: int = 0, n: int | None = None,
+                key_offset: int = 0, prune: bool = True, table=DEFAULT_THROUGHPUT,
+                scale: float = 1.0, to_host: bool = True):
+    """One occx_score_space_host call for a packed space: the description
+    goes H2D, K1 + feature table + K2i over [begin, begin+n) + K3 run on the
+    current stream.  to_host: returns (decoded segments, u64 keys [n_seg,
+    k] host array); else (None, device int64 [n_seg, k] view) without a
+    wait (the all-gather path)."""
+    torch = _torch()
+    n = pk.total - begin if n is None else n
+    lib, ctx = _lib.load(), _lib.ctx()
+    nb, topk_off = ctypes_u64(), ctypes_u64()
+    _lib.check(lib.occx_space_buf_bytes(ctx, len(pk.blob), pk.n_var, pk.n_arch, pk.n_seg,
+                                        pk.k, nb.ref(), topk_off.ref()), "occx_space_buf_bytes")
+    d_buf = _empty(nb.value)
+    h_keys = np.empty((pk.n_seg, pk.k), np.uint64) if to_host else None
+    blob_c = (ctypes.c_char * len(pk.blob)).from_buffer(pk.blob)
+    _lib.check(lib.occx_score_space_host(
+        ctx, pk.h_archs.ctypes.data, pk.n_arch, ctypes.addressof(blob_c), len(pk.blob),
+        (ctypes.c_uint64 * 5)(*pk.offsets), pk.n_seg, pk.n_pool, pk.n_var,
+        table.cpi_matrix().ctypes.data, float(scale), SUM_MODE, begin, n, key_offset,
+        MODE_CODE[Mode(mode)], 0 if prune else _lib.SCORE_EVERY_KEY, pk.k, d_buf.data_ptr(),
+        nb.value, h_keys.ctypes.data if to_host else None, _lib.stream_ptr()),
+        "occx_score_space_host")
+    if to_host:
+        return pk.decode(h_keys), h_keys
+    off = topk_off.value
+    return None, d_buf[off:off + 8 * pk.n_seg * pk.k].view(torch.int64).view(pk.n_seg, pk.k)

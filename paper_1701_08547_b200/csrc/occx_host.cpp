@@ -7,7 +7,7 @@
 // InstructionMix dicts, Ranked entries); this module does them in C++:
 //
 //   pack_plan(dims, var_counts, mixes, tstars, device_id, DeviceError)
-//       -> (blob: bytearray, offsets: 5-tuple, total, n_pool)
+//       -> (blob: bytearray, offsets: 5-tuple, total, n_pool, seg_start list)
 //     the same bytes ScorePlan.__init__ built with numpy (include/occx.h
 //     occx_segdesc_t rows | u32 value pool | u64 masks[n_seg][3] | u32
 //     var_kernel | occx_mix_t rows, each part 256-byte aligned), with the
@@ -293,9 +293,17 @@ PyObject* pack_plan(PyObject*, PyObject* args) {
     const uint32_t n_instr = (uint32_t)std::min<uint64_t>(total, kU32Max);
     std::memcpy(row + 136, &n_instr, 4);
   }
-  PyObject* res = Py_BuildValue("O(nnnnn)Kn", blob, (Py_ssize_t)offs[0], (Py_ssize_t)offs[1],
+  PyObject* starts = PyList_New((Py_ssize_t)n_seg);
+  if (!starts) return fail();
+  owned.push_back(starts);
+  for (size_t i = 0; i < n_seg; ++i) {
+    PyObject* v = PyLong_FromUnsignedLongLong(seg_desc_words[i * (kSegDescBytes / 8)]);
+    if (!v) return fail();
+    PyList_SET_ITEM(starts, (Py_ssize_t)i, v);
+  }
+  PyObject* res = Py_BuildValue("O(nnnnn)KnO", blob, (Py_ssize_t)offs[0], (Py_ssize_t)offs[1],
                                 (Py_ssize_t)offs[2], (Py_ssize_t)offs[3], (Py_ssize_t)offs[4],
-                                (unsigned long long)start, (Py_ssize_t)pool.size());
+                                (unsigned long long)start, (Py_ssize_t)pool.size(), starts);
   fail();   // drop our references (blob is held by res)
   return res;
 }
@@ -441,7 +449,7 @@ done:
 PyMethodDef kMethods[] = {
     {"pack_plan", pack_plan, METH_VARARGS,
      "pack_plan(dims, var_counts, mixes, tstars, device_id, DeviceError) -> "
-     "(blob, offsets, total, n_pool)"},
+     "(blob, offsets, total, n_pool, seg_start)"},
     {"decode", decode, METH_VARARGS,
      "decode(keys, n_arch, k, total, seg_start, kern_dims, var_base) -> [[Ranked]]"},
     {nullptr, nullptr, 0, nullptr}};

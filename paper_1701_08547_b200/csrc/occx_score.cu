@@ -383,11 +383,18 @@ __device__ __forceinline__ void k2_process4(const K2Shared& s, K2Cache& cc, Warp
   }
   // branch-free filter (bitwise on bools: no short-circuit branches); a
   // legal key has bit 63 set, so its high word alone says "non-zero"
-  const uint64_t thr = wl.thr;
+  // High words only: every key already in the warp list comes from an earlier
+  // (lower-index) batch of this warp's forward walk, so a key whose high
+  // word equals the list threshold's has a smaller inverse index and is
+  // below it.  (Feeds whose walk can step back -- a stolen tile -- flush the
+  // warp list first.)  wl_offer compares the full keys.
+  const uint32_t thr_hi = (uint32_t)(wl.thr >> 32);
   bool any = false;
 #pragma unroll
-  for (int j = 0; j < 4; ++j)
-    any = any | (((uint32_t)(key[j] >> 32) != 0u) & ((seg[j] != wl.seg) | (key[j] > thr)));
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t h = (uint32_t)(key[j] >> 32);
+    any = any | ((h != 0u) & ((seg[j] != wl.seg) | (h > thr_hi)));
+  }
   if (__any_sync(0xffffffffu, any)) {
 #ifdef OCCX_K2_TIMING
     const long long c0 = k2_clk();
@@ -1048,6 +1055,7 @@ namespace {
 // consumers in the stage's tile_of slot; kTileEnd ends the CTA's work.  The
 // last CTA to finish returns the counters to zero for the next launch.
 constexpr uint32_t kTileEnd = 0xffffffffu;
+constexpr uint32_t kTileStolen = 0x80000000u;   // tile_of flag: the walk jumps (flush lists)
 constexpr uint32_t kOwnBatch = 4, kStealBatch = 2;
 
 template <int MODE, bool VT_SMEM, int SL>
@@ -1108,7 +1116,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
       if (t0 < len) {
         cur = v * per + t0;
         cur_hi = v * per + min(t0 + kStealBatch, len);
-        return cur++;
+        return kTileStolen | cur++;
       }
     }
     steal_done = true;
@@ -1118,7 +1126,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
   if (threadIdx.x == 0) g_k2_timing[blockIdx.x * 8 + 0] = k2_gt();
 #endif
   // issue tile `tile` into stage st (or the end marker)
-  auto issue = [&](uint32_t st, uint32_t tile) {     // warp 0; lane 0 issues
+  auto issue = [&](uint32_t st, uint32_t tagged) {   // warp 0; lane 0 issues
+    const uint32_t tile = tagged & ~kTileStolen;
     if (tile >= n_tiles) {
       if (lane == 0) {
         tile_of[st] = kTileEnd;
@@ -1128,7 +1137,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
       return;
     }
     if (lane == 0) {
-      tile_of[st] = tile;
+      tile_of[st] = tagged;
       const uint64_t tb = (uint64_t)tile * kTmaTile;
       const uint32_t cnt = (uint32_t)min((uint64_t)kTmaTile, p.n - tb);
       mbar_expect_tx(&full[st], cnt * 16u);
@@ -1189,8 +1198,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
 #ifdef OCCX_K2_TIMING
       K2_ADD(7, k2_clk() - w0);
 #endif
-      const uint32_t tile = tile_of[st];
-      if (tile == kTileEnd) break;
+      const uint32_t tagged = tile_of[st];
+      if (tagged == kTileEnd) break;
+      const uint32_t tile = tagged & ~kTileStolen;
+      if (tagged & kTileStolen) wl_flush(wl, lane, p.k, s.thr, s.list, s.lock);
       const uint64_t tb = (uint64_t)tile * kTmaTile;
       const uint32_t cnt = (uint32_t)min((uint64_t)kTmaTile, p.n - tb);
       const uint4* ring_tile = ring + (size_t)st * kTmaTile;
@@ -1707,6 +1718,94 @@ extern "C" int occx_build_vtab(const occx_ctx* ctx, const occx_mixsum_t* d_sum,
                       reinterpret_cast<cudaStream_t>(stream)>>>(d_sum, d_feat, n_var, n_arch,
                                                                 d_var_kernel, d_segmask, d_vtab);
   OCCX_CUDA_TRY(cudaGetLastError());
+  return OCCX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// score_space() in one call: H2D description -> K1 -> feature table -> K2i ->
+// K3 -> D2H.  d_buf: blob | K1 sums | K1 features | feature table | K2
+// workspace | top-k table, each 256-byte aligned.
+// ---------------------------------------------------------------------------
+static uint64_t align256(uint64_t b) { return (b + 255) / 256 * 256; }
+
+struct SpaceBuf {
+  uint64_t sum, feat, vtab, ws, ws_bytes, topk, total;
+};
+
+static int space_buf_layout(const occx_ctx* ctx, uint64_t blob_bytes, uint32_t n_var,
+                            uint32_t n_arch, uint32_t n_seg, uint32_t k, SpaceBuf* b) {
+  if (!ctx || k == 0 || k > OCCX_MAX_K || n_seg == 0 || n_arch == 0) return OCCX_ERR_VALUE;
+  uint64_t ws = 0;
+  occx_score_workspace_bytes(ctx, n_seg, k, &ws);
+  const uint64_t cells = (uint64_t)n_var * n_arch;
+  b->sum = align256(blob_bytes);
+  b->feat = b->sum + align256((uint64_t)n_var * sizeof(occx_mixsum_t));
+  b->vtab = b->feat + align256(cells * sizeof(occx_feat_t));
+  b->ws = b->vtab + align256(cells * sizeof(occx_vent_t));
+  b->ws_bytes = ws;
+  b->topk = b->ws + align256(ws);
+  b->total = b->topk + align256((uint64_t)n_seg * k * 8);
+  return OCCX_OK;
+}
+
+extern "C" int occx_space_buf_bytes(const occx_ctx* ctx, uint64_t blob_bytes, uint32_t n_var,
+                                    uint32_t n_arch, uint32_t n_seg, uint32_t k,
+                                    uint64_t* bytes, uint64_t* topk_off) {
+  SpaceBuf b;
+  const int st = space_buf_layout(ctx, blob_bytes, n_var, n_arch, n_seg, k, &b);
+  if (st) return st;
+  if (bytes) *bytes = b.total;
+  if (topk_off) *topk_off = b.topk;
+  return OCCX_OK;
+}
+
+extern "C" int occx_score_space_host(const occx_ctx* ctx, const occx_arch_t* h_archs, int n_arch,
+                                     const void* h_blob, uint64_t blob_bytes,
+                                     const uint64_t* blob_off, uint32_t n_seg, uint32_t n_pool,
+                                     uint32_t n_var, const double* h_cpi, double scale,
+                                     int sum_mode, uint64_t begin, uint64_t n,
+                                     uint64_t key_offset, int mode, uint32_t flags, uint32_t k,
+                                     void* d_buf, uint64_t buf_bytes, uint64_t* h_topk,
+                                     void* stream) {
+  if (!ctx || !h_archs || !h_blob || !blob_off || !h_cpi || !d_buf || n_arch < 1 ||
+      n_arch > kMaxArchs || n_var == 0)
+    return OCCX_ERR_VALUE;
+  for (int i = 0; i < 5; ++i)
+    if (blob_off[i] > blob_bytes || (blob_off[i] & 15u)) return OCCX_ERR_VALUE;
+  if ((uint64_t)n_seg % (uint64_t)n_arch) return OCCX_ERR_VALUE;
+  SpaceBuf b;
+  int st = space_buf_layout(ctx, blob_bytes, n_var, (uint32_t)n_arch, n_seg, k, &b);
+  if (st) return st;
+  if (buf_bytes < b.total) return OCCX_ERR_VALUE;
+  int bad;
+  st = occx_check_archs(h_archs, n_arch, &bad);
+  if (st) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* base = static_cast<char*>(d_buf);
+  OCCX_CUDA_TRY(cudaMemcpyAsync(base, h_blob, blob_bytes, cudaMemcpyHostToDevice, s));
+  // the record scorer's scheduler block stays zero (this path uses K2i only)
+  int32_t cols[kMaxArchs];
+  for (int i = 0; i < n_arch; ++i) cols[i] = h_archs[i].cost_key;
+  auto at = [&](int i) { return base + blob_off[i]; };
+  occx_mixsum_t* d_sum = reinterpret_cast<occx_mixsum_t*>(base + b.sum);
+  occx_feat_t* d_feat = reinterpret_cast<occx_feat_t*>(base + b.feat);
+  occx_vent_t* d_vtab = reinterpret_cast<occx_vent_t*>(base + b.vtab);
+  st = occx_feature_score(ctx, reinterpret_cast<const occx_mix_t*>(at(4)), n_var, cols,
+                          (uint32_t)n_arch, h_cpi, scale, sum_mode, d_sum, d_feat, stream);
+  if (st) return st;
+  st = occx_build_vtab(ctx, d_sum, d_feat, n_var, (uint32_t)n_arch,
+                       reinterpret_cast<const uint32_t*>(at(3)),
+                       reinterpret_cast<const uint64_t*>(at(2)), d_vtab, stream);
+  if (st) return st;
+  uint64_t* d_topk = reinterpret_cast<uint64_t*>(base + b.topk);
+  st = occx_score_space(ctx, h_archs, n_arch, reinterpret_cast<const occx_segdesc_t*>(at(0)),
+                        n_seg, reinterpret_cast<const uint32_t*>(at(1)), n_pool, begin, n,
+                        key_offset, mode, flags, d_vtab, n_var, n_seg, k, base + b.ws,
+                        b.ws_bytes, d_topk, stream);
+  if (st) return st;
+  if (h_topk == nullptr) return OCCX_OK;
+  OCCX_CUDA_TRY(cudaMemcpyAsync(h_topk, d_topk, (size_t)n_seg * k * 8, cudaMemcpyDeviceToHost, s));
+  OCCX_CUDA_TRY(cudaStreamSynchronize(s));
   return OCCX_OK;
 }
 

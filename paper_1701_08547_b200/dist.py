@@ -14,6 +14,8 @@ from __future__ import annotations
 
 from typing import Callable
 
+import numpy as np
+
 
 def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
     """[begin, end) of rank's contiguous shard; sizes differ by at most one."""
@@ -58,25 +60,30 @@ def score_space_multi(kernels, archs, mode="corrected", k: int = 16, group=None,
     ``gather_on_host``: all-gather host tensors (gloo transport).
     ``prune=False``: evaluate every candidate's key (same result)."""
     import torch.distributed as dist
-    from .batch import ScorePlan
+    from .batch import _SpacePack, merge_tables, space_score
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    plan = ScorePlan(kernels, archs, mode, k)
+    pk = _SpacePack(kernels, archs, k)
     if scaling == "weak":
-        local = plan.score_implicit(0, plan.total, key_offset=rank * plan.total, prune=prune)
+        begin, n, key_offset = 0, pk.total, rank * pk.total
     elif scaling == "strong":
-        begin, end = shard_range(plan.total, rank, world)
-        local = plan.score_implicit(begin, end - begin, prune=prune)
+        begin, end = shard_range(pk.total, rank, world)
+        n, key_offset = end - begin, 0
     else:
         raise ValueError("scaling must be 'strong' or 'weak'")
-    if world > 1:
-        if gather_on_host:
-            local = allgather_merge(local.cpu(), lambda g: plan.merge(g.cuda(), g.shape[0]),
-                                    group)
-        else:
-            local = allgather_merge(local, lambda g: plan.merge(g, g.shape[0]), group)
-    keys = local.cpu()
-    return plan.decode(keys), keys
+    if world == 1:
+        segs, keys = space_score(pk, mode, begin, n, key_offset, prune=prune)
+        return segs, keys
+    _, local = space_score(pk, mode, begin, n, key_offset, prune=prune, to_host=False)
+
+    def merge(g):
+        return merge_tables(g, g.shape[0], pk.n_seg, pk.k)
+    if gather_on_host:
+        local = allgather_merge(local.cpu(), lambda g: merge(g.cuda()), group)
+    else:
+        local = allgather_merge(local, merge, group)
+    keys = local.cpu().numpy().view(np.uint64)
+    return pk.decode(keys), keys
 
 
 def score_space_sharded(plan, group=None, records=None, stream=None):

@@ -471,6 +471,30 @@ def test_k2i_many_segments_and_score_space(P, torch):
     assert [e.key for e in res[0].entries] == [int(x) for x in want[0] if x]
 
 
+def test_score_space_one_call_equals_plan(P, torch):
+    """occx_score_space_host (the one-call score_space() path: H2D, K1,
+    feature table, K2i, K3, D2H) == ScorePlan's step-by-step K2i table on
+    config 4 windows, weak-scaling key offsets, both prune settings, both
+    modes; the device-resident (to_host=False) table too."""
+    from paper_1701_08547_b200 import workloads
+    from paper_1701_08547_b200.batch import _SpacePack, space_score
+    cfg = workloads.config4()
+    for mode in ("corrected", "verbatim"):
+        plan = P.ScorePlan(cfg.kernels, cfg.archs, mode, k=cfg.k)
+        pk = _SpacePack(cfg.kernels, cfg.archs, cfg.k)
+        for begin, n, off, prune in ((0, plan.total, 0, True), (0, plan.total, 0, False),
+                                     (12345, 7_000_001, 0, True),
+                                     (0, plan.total, plan.total, False)):
+            want = plan.score_implicit(begin, n, key_offset=off,
+                                       prune=prune).cpu().numpy().view(np.uint64)
+            segs, keys = space_score(pk, mode, begin, n, off, prune=prune)
+            assert np.array_equal(keys, want), (mode, begin, n, off, prune)
+            _, dev = space_score(pk, mode, begin, n, off, prune=prune, to_host=False)
+            assert np.array_equal(dev.cpu().numpy().view(np.uint64), want)
+            assert [[e.key for e in sg.entries] for sg in segs] == \
+                [[int(x) for x in row if x] for row in want]
+
+
 # ---------------------------------------------------------------------------
 # multi-process sharding with real GPU kernels (gloo transport; NCCL on 2-8 GPUs)
 # ---------------------------------------------------------------------------

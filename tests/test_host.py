@@ -265,8 +265,9 @@ def _check_native_pack(kernels, archs):
     import numpy as np
     from paper_1701_08547_b200 import _lib
     rows, pool, masks, vk, mix, total = _py_pack(kernels, archs)
-    blob, offs, n_total, n_pool = _native_pack(kernels, archs)
+    blob, offs, n_total, n_pool, starts = _native_pack(kernels, archs)
     assert n_total == total and n_pool == max(len(pool), 1)
+    assert starts == [r[0] for r in rows]
     n_seg = len(rows)
     desc = np.frombuffer(blob, _lib.SEGDESC, n_seg, offs[0])
     for d, (st, size, a, vb, o, ln) in zip(desc, rows):
