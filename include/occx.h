@@ -123,7 +123,10 @@ typedef struct occx_mix_t {
   uint32_t counts[16];
   uint32_t first_key[16];
   uint64_t reg_operands;
-  uint32_t n_instr, reserved;
+  uint32_t n_instr;
+  uint32_t reserved;      /* K0 status: OCCX_ERR_CAPACITY when the call holds
+                             >= 2^32 records or the kernel >= 2^29 (nothing
+                             else of the row is meaningful then), else 0   */
 } occx_mix_t;
 
 /* Per-mix sums: flops/mem/ctrl (mix.py:213-223) and intensity (:333-337). */

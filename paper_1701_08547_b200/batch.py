@@ -328,6 +328,9 @@ def mix_reduce(d_instr, d_off, n_kernels: int, d_lut, n_sig: int, d_out=None):
 
 def mix_from_record(m) -> InstructionMix:
     """occx_mix_t -> InstructionMix with dict insertion order restored."""
+    if int(m["reserved"]):
+        raise DeviceError("instruction stream too long for the mix reducer "
+                          "(>= 2^29 instructions in a kernel or 2^32 in a call)")
     present = [(int(m["first_key"][c]), c) for c in range(15) if m["counts"][c]]
     present.sort()
     counts = {COUNTABLE[c]: int(m["counts"][c]) for _, c in present}

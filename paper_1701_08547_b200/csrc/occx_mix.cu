@@ -49,6 +49,7 @@ constexpr int kFlushPieces = 255 / 8;                 // byte counters cannot ov
 constexpr uint32_t kPred = 11;                        // OpClass.PREDICATE device id
 constexpr uint32_t kAbsent = 0xffffffffu;
 constexpr uint32_t kNullLv = 0x7cu;                   // class 15, shift 124: counts nothing
+constexpr uint32_t kMaxKernelRecords = 1u << 29;      // positions (2 * pos) and lane sums fit u32
 #ifndef OCCX_K0_LDS
 #define OCCX_K0_LDS 6
 #endif
@@ -218,7 +219,11 @@ __device__ __forceinline__ void finish_kernel(MixAcc& a, uint32_t* my_first, occ
   if (lane == (int)kPred && gfirst < first) first = gfirst;
   if (lane < 17) my_first[lane] = kAbsent;               // reset for the warp's next kernel
   __syncwarp();
-  const uint32_t reg_total = __reduce_add_sync(0xffffffffu, a.regs);
+  // 64-bit total from two 16-bit-half warp sums (a lane's u32 cannot wrap:
+  // kernels are < 2^29 records, <= 255 operands each, 1/32 of them per lane)
+  const uint64_t reg_total =
+      (uint64_t)__reduce_add_sync(0xffffffffu, a.regs & 0xffffu) +
+      ((uint64_t)__reduce_add_sync(0xffffffffu, a.regs >> 16) << 16);
   if (lane < 16) {
     o->counts[lane] = lane < 15 ? a.total : 0u;
     o->first_key[lane] = (lane < 15 && a.total) ? first : kAbsent;
@@ -226,7 +231,7 @@ __device__ __forceinline__ void finish_kernel(MixAcc& a, uint32_t* my_first, occ
   if (lane == 0) {
     o->reg_operands = reg_total;
     o->n_instr = n_instr;
-    o->reserved = 0;
+    o->reserved = n_instr >= kMaxKernelRecords ? (uint32_t)OCCX_ERR_CAPACITY : 0u;
   }
   a = MixAcc{};
 }
@@ -258,6 +263,14 @@ __global__ void __launch_bounds__(kMixThreads, 1) mix_reduce_kernel(const __grid
 
   // this warp's kernel run [ks, ke): half-warp 0 searches bound(gw), half 1 bound(gw + 1)
   const uint64_t base = __ldg(p.off), n_rec = __ldg(p.off + p.n_kernels) - base;
+  if (n_rec >> 32) {              // positions are u32: flag every kernel, count nothing
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < p.n_kernels;
+         k += gridDim.x * blockDim.x) {
+      p.out[k].n_instr = 0;
+      p.out[k].reserved = (uint32_t)OCCX_ERR_CAPACITY;
+    }
+    return;
+  }
   uint32_t ks, ke;
   {
     const uint32_t w = gw + (uint32_t)(lane >> 4);

@@ -1177,6 +1177,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
     for (uint32_t t = issued; !ended; ++t) {
       const uint32_t st = t % kTmaStages;
       mbar_wait(&empty[st], ((t / kTmaStages) & 1u) ^ 1u);
+      // the consumers' generic-proxy reads of this slot (ordered before
+      // their empty arrivals) precede the async-proxy TMA write into it
+      if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(st, next);
       if (!ended) next = grab();
       issued = t + 1;

@@ -88,6 +88,18 @@ def main():
                   f"{mmm(setup)}; consumers done {mmm(cons)}; end {mmm(end)}")
             print(f"   per CTA: setup {mmm(setup - ent)}; stream {mmm(cons - setup)}; "
                   f"merge+flush {mmm(end - cons)}")
+            cnt = np.zeros(8 * 1024, np.uint64)
+            plan.score_partials(rec, n, index_base=begin)
+            torch.cuda.synchronize()
+            lib.occx_debug_k2_counts(ctypes.c_void_p(cnt.ctypes.data), 1024, 1)
+            plan.score_partials(rec, n, index_base=begin)
+            torch.cuda.synchronize()
+            lib.occx_debug_k2_counts(ctypes.c_void_p(cnt.ctypes.data), 1024, 1)
+            c = cnt.reshape(-1, 8)[: plan.grid_lists].sum(axis=0)
+            print(f"   per launch: offers {c[0]} (per 1M cand {c[0] / n * 1e6:.0f}), batch merges "
+                  f"{c[1]}, segment flushes {c[2]}, mixed batches {c[3]}, CTA inserts {c[4]}, "
+                  f"cache fills {c[5]} ({c[5] / n * 1e6:.0f}/M), offer cycles {c[6] / max(c[0], 1):.0f}"
+                  f"/offer, full-wait cycles/warp {c[7] / plan.grid_lists / 16:.0f}")
             dur = cons - setup
             slow = np.argsort(dur)[-8:]
             print("   slowest streams (blk:us:tiles):",

@@ -112,3 +112,32 @@ def test_ctx_options_same_topk(env, options):
         assert plan.grid_lists == 2 * lib.occx_ctx_sm_count(h)
     got = plan.score(plan.generate(), plan.total).cpu().numpy().view(np.uint64)
     assert got.reshape(plan.n_seg, plan.k).tolist() == load_golden("topk_config2.json")["corrected"]
+
+
+def test_k0_capacity_flags_and_64bit_register_operands(env):
+    """K0 (ref mix.py:245-261, Python ints are unbounded): a kernel whose
+    register operands sum past 2^32 is exact (64-bit total); a call whose
+    offsets span >= 2^32 records or a kernel >= 2^29 records is flagged
+    OCCX_ERR_CAPACITY per row (mix_from_record raises) instead of wrapping."""
+    from paper_1701_08547_b200 import batch, _lib as L2
+    from paper_1701_08547_b200.errors import DeviceError
+    torch, L, lib, _, _ = env
+    n = 17_000_000                                    # 255 * n > 2^32
+    rec = torch.full((n,), (255 << 17) | (3 << 1), dtype=torch.int32, device="cuda")
+    off = batch._to_device(np.asarray([0, n], np.uint64))
+    lut = batch._to_device(batch.CLASS_LUT)
+    out = batch._to_host(batch.mix_reduce(rec, off, 1, lut, len(batch.CLASS_LUT)), L2.MIX, 1)
+    assert int(out[0]["reg_operands"]) == 255 * n and int(out[0]["counts"][3]) == n
+    assert int(out[0]["reserved"]) == 0
+    # a call spanning 2^32 records: flagged before any record is read
+    off = batch._to_device(np.asarray([0, 5, 1 << 32], np.uint64))
+    out = batch._to_host(batch.mix_reduce(rec, off, 2, lut, len(batch.CLASS_LUT)), L2.MIX, 2)
+    assert out["reserved"].tolist() == [8, 8]
+    with pytest.raises(DeviceError):
+        batch.mix_from_record(out[0])
+    # one kernel of 2^29 records (2 GB): flagged; its neighbour is not
+    big = torch.zeros((1 << 29) + 64, dtype=torch.int32, device="cuda")
+    off = batch._to_device(np.asarray([0, 64, 64 + (1 << 29)], np.uint64))
+    out = batch._to_host(batch.mix_reduce(big, off, 2, lut, len(batch.CLASS_LUT)), L2.MIX, 2)
+    assert out["reserved"].tolist() == [0, 8] and int(out[0]["counts"][0]) == 64
+    del big
