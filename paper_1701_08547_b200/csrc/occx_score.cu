@@ -786,8 +786,9 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
     if (sb.ns >= 4) {              // at most one REGS step among the lane's four
       const uint32_t t0 = lds_u32(tr + 4u * ri), t1 = lds_u32(tr + 4u * ri + 4u);
       const uint32_t sa = sb.ts + 4u * si;
+      const int jb = (int)(sb.ns - si);       // first j in the next REGS row
 #pragma unroll
-      for (int j = 0; j < 4; ++j) v[j] = min(si + j < sb.ns ? t0 : t1, lds_u32(sa + 4u * j));
+      for (int j = 0; j < 4; ++j) v[j] = min(j < jb ? t0 : t1, lds_u32(sa + 4u * j));
     } else {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -831,8 +832,9 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
       const uint32_t r0 = fastdiv(o8, sb.ds), s0 = o8 - r0 * sb.ns;
       const uint32_t t0 = lds_u32(tr + 4u * r0), t1 = lds_u32(tr + 4u * r0 + 4u);
       const uint32_t sa = sb.ts + 4u * s0;
+      const int jb = (int)(sb.ns - s0);       // first j in the next REGS row
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = min(s0 + j < sb.ns ? t0 : t1, lds_u32(sa + 4u * j));
+      for (int j = 0; j < 8; ++j) v[j] = min(j < jb ? t0 : t1, lds_u32(sa + 4u * j));
     } else {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -863,8 +865,9 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
       const uint32_t r0 = fastdiv(o8, sb.ds), s0 = o8 - r0 * sb.ns;
       const uint32_t t0 = lds_u32(tr + 4u * r0), t1 = lds_u32(tr + 4u * r0 + 4u);
       const uint32_t sa = sb.ts + 4u * s0;
+      const int jb = (int)(sb.ns - s0);       // first j in the next REGS row
 #pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = min(s0 + j < sb.ns ? t0 : t1, lds_u32(sa + 4u * j));
+      for (int j = 0; j < 16; ++j) v[j] = min(j < jb ? t0 : t1, lds_u32(sa + 4u * j));
     } else {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
