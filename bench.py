@@ -472,6 +472,34 @@ def secondary_config3_e2e(n_kernels: int = 1000, reps: int = 5):
                                        f"oracle/pyref.aggregate, {wall:.2f} s wall"}}
 
 
+def secondary_scalar_api(reps: int = 300):
+    """The reference's scalar entry points called one at a time (a caller
+    looping over the drop-in API): every call is a batch of one -- pack, H2D,
+    one launch, D2H, synchronize -- with no CPU fallback.  Per-call latency
+    beside the reference's measured 5.27 us per occupancy() call (SURVEY
+    §6, one core)."""
+    import paper_1701_08547_b200 as P
+    k20 = P.builtin_arch("kepler")
+    mix = P.InstructionMix({P.OpClass.FP32: 17, P.OpClass.LOAD_STORE: 5}, 63)
+    res = P.KernelResources("atax", 27)
+    calls = {"occupancy": lambda: P.occupancy(k20, P.LaunchInput(128, 27)),
+             "cost_estimate": lambda: P.cost_estimate(mix, 3.5),
+             "suggest": lambda: P.suggest(k20, res)}
+    out = {}
+    for name, fn in calls.items():
+        for _ in range(20):
+            fn()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        out[name] = {"us_per_call": (time.perf_counter() - t0) / reps * 1e6}
+    out["reference_us_per_call"] = {"occupancy": 5.27, "cost_estimate": 12.2,
+                                    "source": "SURVEY §6 / §8(a), one core, Python 3.12"}
+    out["note"] = ("a batch of one per call (H2D + launch + D2H + sync); the batch "
+                   "entry points are the intended use")
+    return out
+
+
 def secondary_records(name: str, mode: str, hbm_peak: float, steps: int = 20):
     """K2 + K3 on another BASELINE config (inputs resident, > L2 for config 4;
     config 2's 419 MB also exceeds the 126 MB L2)."""
@@ -589,13 +617,13 @@ def secondary_space_api(cfg, mode: str, steps: int = 10):
     out = {"kernel": "score_space_kernel (K2i, implicit grid, no K3)", "kernel_ms": k_ms,
            "value": plan.total / (k_ms / 1e3), "unit": UNIT, "bound": "integer issue",
            "note": "every candidate's key evaluated (prune=False); no candidate records "
-                   "in HBM; see profiles/r01_k2i_ncu_full.json",
+                   "in HBM; see profiles/r02_k2i_ncu_full.json",
            "pruned": {"kernel_ms": p_ms, "value": plan.total / (p_ms / 1e3),
                       "note": "library default: blocks skipped on an exact bound"}}
     # issue roofline: the ncu capture's warp-instruction count per launch (same
     # workload) over the live kernel time, against 4 issue slots/SM/clock
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_k2i_ncu_full.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r02_k2i_ncu_full.json")) as fh:
             prof = json.load(fh)
         if prof.get("workload") == cfg.name:
             import pynvml
@@ -608,7 +636,10 @@ def secondary_space_api(cfg, mode: str, steps: int = 10):
             out["roofline"] = {"bound": "issue", "achieved": achieved, "peak": peak,
                                "unit": "G warp-instructions/s", "frac": achieved / peak,
                                "instructions_per_launch": prof["warp_instructions"],
-                               "peak_source": f"4 issue slots x {sms} SMs x {mhz} MHz (max SM clock)"}
+                               "peak_source": f"4 issue slots x {sms} SMs x {mhz} MHz (max SM clock)",
+                               "alu_pipe_pct_ncu": prof.get("alu_pipe_pct"),
+                               "note": "the ALU pipe (ISETP/SEL/VIMNMX/LOP3) is the tighter "
+                                       "limit: alu_pipe_pct_ncu from the committed capture"}
     except Exception as exc:
         out["roofline"] = {"error": repr(exc)[:160]}
     return out
@@ -651,6 +682,22 @@ def golden_topk(workload: str, mode: str):
             return json.load(fh).get(mode)
     except OSError:
         return None
+
+
+def workload_config(cfg, n_seg: int, k: int, mode: str, world: int, scaling: str,
+                    gloo: bool = False) -> dict:
+    """The `config` object both arms print (the same workload, the same keys)."""
+    from paper_1701_08547_b200 import workloads
+    total = cfg.total * (world if scaling == "weak" else 1)
+    per_gpu = cfg.total if scaling == "weak" else -(-cfg.total // world)
+    shard = ("each GPU scores its own copy of the space" if scaling == "weak"
+             else "index-range shards of one space")
+    return {"workload": cfg.name, "candidates": total, "candidates_per_gpu": per_gpu,
+            "segments": n_seg, "k": k, "mode": mode, "record_bytes": 16,
+            "kernels": list(workloads.KERNEL_NAMES), "archs": [a.name for a in cfg.archs],
+            "parallelism": f"{shard} x{world} + {'gloo' if gloo else 'NCCL'} all-gather "
+                           f"top-k + K3 merge",
+            "l2": f"inputs {16 * per_gpu / 1e9:.1f} GB per GPU >> 126 MB L2; no flush"}
 
 
 def main():
@@ -702,7 +749,8 @@ def main():
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": None, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "int64 (Python int)", "data": "synthetic",
-            "config": {"workload": cfg.name, "candidates": cfg.total, "mode": args.mode},
+            "config": workload_config(cfg, len(cfg.kernels) * len(cfg.archs), cfg.k, args.mode,
+                                      args.gpus, args.scaling),
             "cpu_baseline": r,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }), flush=True)
@@ -837,7 +885,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         try:
-            e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
+            e2e_steps = args.e2e_steps or max(10, min(args.steps * 2, 40))
             mode = args.mode
 
             def api_step(prune):
@@ -846,7 +894,7 @@ def main():
                                          prune=prune)
 
             def timed_api(prune: bool) -> float:
-                for _ in range(2):
+                for _ in range(5):
                     api_step(prune)
                 torch.cuda.synchronize()
                 barrier()
@@ -914,6 +962,7 @@ def main():
         for name, fn in (("config3_mix_reduce", lambda: secondary_config3(hbm_peak)),
                          ("config3_text_e2e", lambda: secondary_config3_e2e()),
                          ("acceptance_7a_occupancy", lambda: secondary_acceptance_7a(hbm_peak)),
+                         ("scalar_api_latency", lambda: secondary_scalar_api()),
                          ("implicit_grid_score_space", lambda: secondary_space_api(cfg, args.mode)),
                          ("config4_records", lambda: secondary_records("config4", args.mode, hbm_peak)),
                          ("suggest_100k_kernels", lambda: secondary_suggest(args.mode)),
@@ -936,21 +985,13 @@ def main():
     if rank == 0:
         # K2 + K3 per step, + K3 after the all-gather for N > 1
         launches = args.steps * (2 + (1 if world > 1 else 0))
-        shard = ("each GPU scores its own copy of the space" if args.scaling == "weak"
-                 else "index-range shards of one space")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "u32 integer (u64 keys)", "data": "synthetic",
-            "config": {"workload": cfg.name, "candidates": global_total,
-                       "candidates_per_gpu": n, "segments": plan.n_seg,
-                       "k": plan.k, "mode": args.mode, "record_bytes": 16,
-                       "kernels": list(workloads.KERNEL_NAMES),
-                       "archs": [a.name for a in cfg.archs],
-                       "parallelism": f"{shard} x{world} + "
-                                      f"{'gloo' if gloo else 'NCCL'} all-gather top-k + K3 merge",
-                       "l2": f"inputs {16 * n / 1e9:.1f} GB per GPU >> 126 MB L2; no flush"},
+            "config": workload_config(cfg, plan.n_seg, plan.k, args.mode, world, args.scaling,
+                                      gloo),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak,
                          "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                          "kernel": "score_topk_kernel (K2)", "kernel_ms": k2_ms,

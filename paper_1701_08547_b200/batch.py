@@ -677,8 +677,9 @@ class ScorePlan:
             _DevPtr(base + o) for o in offsets)
         self.d_sum, self.d_feat, self.d_vtab, self.d_ws = (_DevPtr(base + o) for o in offs[1:])
         # the workspace's scheduler block starts zeroed (the scorer leaves it zero)
-        tables = self.grid_lists * self.n_seg * k * 8
-        self._d_buf[offs[4] + tables:offs[4] + self.ws_bytes].zero_()
+        _lib.check(_lib.load().occx_score_workspace_init(
+            self._ctx, _lib.ptr(self.d_ws), self.ws_bytes, _lib.stream_ptr()),
+            "occx_score_workspace_init")
         # K1 on device, then the feature table
         cols = [int(a["cost_key"]) for a in self.h_archs]
         feature_records(d_mix, self.n_var, cols, table.cpi_matrix(), scale,

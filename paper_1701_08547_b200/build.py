@@ -38,15 +38,19 @@ def _stale(obj: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, timing: bool = False) -> str:
+def build(verbose: bool = False, timing: bool = False, variant: str = "",
+          defs: tuple = ()) -> str:
     """Compile the stale sources (in parallel) and link liboccx.so.
     ``timing``: the instrumented K2 build (-DOCCX_K2_TIMING: per-CTA
     globaltimer spans and slow-path counters, scripts/k2_profile.py) into
     _objs_timing/liboccx_timing.so -- experiments only, never loaded by
     the package unless OCCX_LIB names it."""
-    build_dir = BUILD + ("_timing" if timing else "")
-    out = os.path.join(build_dir, "liboccx_timing.so") if timing else OUT
-    defs = ["-DOCCX_K2_TIMING"] if timing else []
+    # experiment builds (never loaded unless OCCX_LIB names them): the
+    # instrumented K2 (timing) or a named variant with extra -D flags
+    tag = "_timing" if timing else (f"_{variant}" if variant else "")
+    build_dir = BUILD + tag
+    out = os.path.join(build_dir, f"liboccx{tag}.so") if tag else OUT
+    defs = (["-DOCCX_K2_TIMING"] if timing else []) + [f"-D{d}" for d in defs]
     os.makedirs(build_dir, exist_ok=True)
     header_deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)
                    if f.endswith((".cuh", ".h"))]
@@ -76,7 +80,7 @@ def build(verbose: bool = False, timing: bool = False) -> str:
             failed.append(src)
     if failed:
         raise RuntimeError(f"compile failed on {', '.join(failed)}")
-    if not timing:        # the native host module (CPython extension, csrc/occx_host.cpp)
+    if not tag:           # the native host module (CPython extension, csrc/occx_host.cpp)
         import sysconfig
         ext = os.path.join(HERE, "_occx_host" + sysconfig.get_config_var("EXT_SUFFIX"))
         src = os.path.join(CSRC, "occx_host.cpp")
@@ -97,4 +101,6 @@ def build(verbose: bool = False, timing: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, timing="--timing" in sys.argv))
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), "")
+    dd = tuple(a.split("=", 1)[1] for a in sys.argv if a.startswith("--define="))
+    print(build(verbose="-v" in sys.argv, timing="--timing" in sys.argv, variant=var, defs=dd))

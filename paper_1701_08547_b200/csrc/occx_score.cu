@@ -388,13 +388,20 @@ __device__ __forceinline__ void k2_process4(const K2Shared& s, K2Cache& cc, Warp
   // word equals the list threshold's has a smaller inverse index and is
   // below it.  (Feeds whose walk can step back -- a stolen tile -- flush the
   // warp list first.)  wl_offer compares the full keys.
-  const uint32_t thr_hi = (uint32_t)(wl.thr >> 32);
   bool any = false;
+#ifdef OCCX_K2_FILTER64
+  const uint64_t thr = wl.thr;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    any = any | (((uint32_t)(key[j] >> 32) != 0u) & ((seg[j] != wl.seg) | (key[j] > thr)));
+#else
+  const uint32_t thr_hi = (uint32_t)(wl.thr >> 32);
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const uint32_t h = (uint32_t)(key[j] >> 32);
     any = any | ((h != 0u) & ((seg[j] != wl.seg) | (h > thr_hi)));
   }
+#endif
   if (__any_sync(0xffffffffu, any)) {
 #ifdef OCCX_K2_TIMING
     const long long c0 = k2_clk();
@@ -1594,6 +1601,16 @@ extern "C" int occx_score_workspace_bytes(const occx_ctx* ctx, uint32_t n_seg, u
 }
 
 extern "C" int occx_score_lists(const occx_ctx* ctx) { return ctx ? score_grid(ctx) : 0; }
+
+extern "C" int occx_score_workspace_init(const occx_ctx* ctx, void* d_ws, uint64_t ws_bytes,
+                                         void* stream) {
+  if (!ctx || !d_ws) return OCCX_ERR_VALUE;
+  const uint64_t sb = sched_bytes(ctx);
+  if (ws_bytes < sb) return OCCX_ERR_VALUE;
+  OCCX_CUDA_TRY(cudaMemsetAsync(static_cast<char*>(d_ws) + (ws_bytes - sb), 0, sb,
+                                reinterpret_cast<cudaStream_t>(stream)));
+  return OCCX_OK;
+}
 
 extern "C" int occx_topk_merge(const occx_ctx* ctx, const uint64_t* d_lists, uint32_t n_lists,
                                uint32_t n_seg, uint32_t k, uint64_t* d_out, void* stream) {
