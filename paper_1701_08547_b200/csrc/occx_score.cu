@@ -1241,10 +1241,20 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
 #ifdef OCCX_K2_TIMING
       const long long p0 = k2_clk();
 #endif
+#ifdef OCCX_K2_STREAM_ONLY
+      // experiment build: stream the records, fold them into one word, no scoring
+      uint32_t fold = 0;
+#pragma unroll
+      for (int h = 0; h < kTmaSlices; ++h)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) fold ^= r[h][j].x ^ r[h][j].y ^ r[h][j].z ^ r[h][j].w;
+      if (fold == 0x9e3779b9u && lane == 0) wl.seg = fold;
+#else
 #pragma unroll
       for (int h = 0; h < kTmaSlices; ++h)
         k2_process4<MODE, VT_SMEM>(s, cc, wl, r[h], kIdxMask - p.index_base - tb - slice - 128u * h,
                                    lane, p.k);
+#endif
 #ifdef OCCX_K2_TIMING
       if (lane == 0)
         atomicAdd(&g_k2_hist[blockIdx.x * 16 + (tile * 16u) / n_tiles], (unsigned long long)(k2_clk() - p0));
