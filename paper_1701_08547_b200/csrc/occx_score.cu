@@ -363,7 +363,7 @@ __device__ inline void k2_flush(const ScoreParams& p, const K2Shared& s) {
 template <int MODE, bool VT_SMEM>
 __device__ __forceinline__ void k2_process4(const K2Shared& s, K2Cache& cc, WarpList& wl,
                                             const uint4 (&r)[4], const uint64_t inv, int lane,
-                                            uint32_t k) {
+                                            uint32_t k, bool exact = false) {
   uint64_t key[4];
   uint32_t seg[4];
   const bool hit = k2_hit(cc, r[0]) & k2_hit(cc, r[1]) & k2_hit(cc, r[2]) & k2_hit(cc, r[3]);
@@ -386,22 +386,21 @@ __device__ __forceinline__ void k2_process4(const K2Shared& s, K2Cache& cc, Warp
   // High words only: every key already in the warp list comes from an earlier
   // (lower-index) batch of this warp's forward walk, so a key whose high
   // word equals the list threshold's has a smaller inverse index and is
-  // below it.  (Feeds whose walk can step back -- a stolen tile -- flush the
-  // warp list first.)  wl_offer compares the full keys.
+  // below it.  Once the walk has stepped back (a stolen tile: `exact`) the
+  // full keys are compared.  wl_offer compares the full keys either way.
   bool any = false;
-#ifdef OCCX_K2_FILTER64
-  const uint64_t thr = wl.thr;
+  if (exact) {
 #pragma unroll
-  for (int j = 0; j < 4; ++j)
-    any = any | (((uint32_t)(key[j] >> 32) != 0u) & ((seg[j] != wl.seg) | (key[j] > thr)));
-#else
-  const uint32_t thr_hi = (uint32_t)(wl.thr >> 32);
+    for (int j = 0; j < 4; ++j)
+      any = any | (((uint32_t)(key[j] >> 32) != 0u) & ((seg[j] != wl.seg) | (key[j] > wl.thr)));
+  } else {
+    const uint32_t thr_hi = (uint32_t)(wl.thr >> 32);
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint32_t h = (uint32_t)(key[j] >> 32);
-    any = any | ((h != 0u) & ((seg[j] != wl.seg) | (h > thr_hi)));
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t h = (uint32_t)(key[j] >> 32);
+      any = any | ((h != 0u) & ((seg[j] != wl.seg) | (h > thr_hi)));
+    }
   }
-#endif
   if (__any_sync(0xffffffffu, any)) {
 #ifdef OCCX_K2_TIMING
     const long long c0 = k2_clk();
@@ -1065,7 +1064,7 @@ namespace {
 // consumers in the stage's tile_of slot; kTileEnd ends the CTA's work.  The
 // last CTA to finish returns the counters to zero for the next launch.
 constexpr uint32_t kTileEnd = 0xffffffffu;
-constexpr uint32_t kTileStolen = 0x80000000u;   // tile_of flag: the walk jumps (flush lists)
+constexpr uint32_t kTileStolen = 0x80000000u;   // tile_of flag: the walk may step back
 constexpr uint32_t kOwnBatch = 4, kStealBatch = 2;
 
 template <int MODE, bool VT_SMEM, int SL>
@@ -1202,6 +1201,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
     K2Cache cc;
     cc.x = cc.z = cc.w = 0xffffffffu;
     k2_fill<VT_SMEM>(s.c, make_uint4(0xffffffffu, 0, 0, 0xffffffffu), cc);
+    bool stepped_back = false;         // a stolen tile came: exact list filter from then on
     for (uint32_t t = 0;; ++t) {
       const uint32_t st = t % kTmaStages;
 #ifdef OCCX_K2_TIMING
@@ -1214,7 +1214,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
       const uint32_t tagged = tile_of[st];
       if (tagged == kTileEnd) break;
       const uint32_t tile = tagged & ~kTileStolen;
-      if (tagged & kTileStolen) wl_flush(wl, lane, p.k, s.thr, s.list, s.lock);
+      stepped_back |= (tagged & kTileStolen) != 0;
       const uint64_t tb = (uint64_t)tile * kTmaTile;
       const uint32_t cnt = (uint32_t)min((uint64_t)kTmaTile, p.n - tb);
       const uint4* ring_tile = ring + (size_t)st * kTmaTile;
@@ -1253,7 +1253,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
 #pragma unroll
       for (int h = 0; h < kTmaSlices; ++h)
         k2_process4<MODE, VT_SMEM>(s, cc, wl, r[h], kIdxMask - p.index_base - tb - slice - 128u * h,
-                                   lane, p.k);
+                                   lane, p.k, stepped_back);
 #endif
 #ifdef OCCX_K2_TIMING
       if (lane == 0)

@@ -47,6 +47,10 @@ def timed(fn, reps=15, do_flush=True):
 
 
 def workload(name):
+    if name.startswith("seg"):               # one segment of config 5: seg<s>
+        cfg = workloads.config5()
+        size = cfg.total // 20
+        return cfg, int(name[3:]) * size, size
     if name == "shard8":
         cfg = workloads.config5()
         total = cfg.total

@@ -141,3 +141,48 @@ def test_k0_capacity_flags_and_64bit_register_operands(env):
     out = batch._to_host(batch.mix_reduce(big, off, 2, lut, len(batch.CLASS_LUT)), L2.MIX, 2)
     assert out["reserved"].tolist() == [0, 8] and int(out[0]["counts"][0]) == 64
     del big
+
+
+def test_workspace_scheduler_block_and_one_call_errors(env):
+    """occx_score_workspace_init zeroes the scheduler block (the record
+    scorer leaves it zero after every call); occx_score_space_host and
+    occx_space_buf_bytes reject bad arguments before launching anything."""
+    import ctypes
+    from paper_1701_08547_b200.batch import _SpacePack
+    torch, L, lib, plan, rec = env
+    ctx = L.ctx()
+    assert lib.occx_score_workspace_init(ctx, None, plan.ws_bytes, L.stream_ptr()) == 1
+    assert lib.occx_score_workspace_init(ctx, L.ptr(plan.d_ws), 16, L.stream_ptr()) == 1
+    ws = torch.full((plan.ws_bytes,), 0x5A, dtype=torch.uint8, device="cuda")
+    assert lib.occx_score_workspace_init(ctx, L.ptr(ws), plan.ws_bytes, L.stream_ptr()) == 0
+    lists = plan.grid_lists * plan.n_seg * plan.k * 8
+    assert int(ws[lists:].sum()) == 0 and int(ws[:lists].min()) == 0x5A
+    out = torch.empty((plan.n_seg, plan.k), dtype=torch.int64, device="cuda")
+    for _ in range(3):                   # the block is zero again after every call
+        assert lib.occx_score_topk(ctx, L.ptr(plan.h_archs), plan.n_arch, L.ptr(rec), plan.total,
+                                   0, 0, L.ptr(plan.d_vtab), plan.n_var, plan.n_seg, plan.k,
+                                   L.ptr(ws), plan.ws_bytes, L.ptr(out), L.stream_ptr()) == 0
+        torch.cuda.synchronize()
+        assert int(ws[lists:].sum()) == 0
+    pk = _SpacePack(plan.kernels, plan.archs, plan.k)
+    nb, off = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    assert lib.occx_space_buf_bytes(ctx, len(pk.blob), pk.n_var, pk.n_arch, pk.n_seg, 0,
+                                    ctypes.byref(nb), ctypes.byref(off)) == 1      # k = 0
+    assert lib.occx_space_buf_bytes(ctx, len(pk.blob), pk.n_var, pk.n_arch, pk.n_seg, pk.k,
+                                    ctypes.byref(nb), ctypes.byref(off)) == 0
+    buf = torch.empty((nb.value,), dtype=torch.uint8, device="cuda")
+    blob = (ctypes.c_char * len(pk.blob)).from_buffer(pk.blob)
+    keys = np.zeros((pk.n_seg, pk.k), np.uint64)
+    cpi = np.zeros((4, 16))
+
+    def call(**kw):
+        a = dict(offs=(ctypes.c_uint64 * 5)(*pk.offsets), buf_bytes=nb.value, n_var=pk.n_var)
+        a.update(kw)
+        return lib.occx_score_space_host(ctx, L.ptr(pk.h_archs), pk.n_arch, ctypes.addressof(blob),
+                                         len(pk.blob), a["offs"], pk.n_seg, pk.n_pool, a["n_var"],
+                                         cpi.ctypes.data, 1.0, 0, 0, pk.total, 0, 0, 0, pk.k,
+                                         L.ptr(buf), a["buf_bytes"], keys.ctypes.data,
+                                         L.stream_ptr())
+    assert call(buf_bytes=nb.value - 1) == 1                   # buffer too small
+    assert call(offs=(ctypes.c_uint64 * 5)(1, 0, 0, 0, 0)) == 1  # misaligned part offset
+    assert call(n_var=0) == 1
