@@ -256,15 +256,16 @@ int occx_build_vtab(const occx_ctx* ctx, const occx_mixsum_t* d_sum,
  * `variant`/`arch` out of range -> candidate excluded.  d_topk == NULL
  * stops after K2: the per-CTA tables stay in d_ws as
  * [occx_score_lists(ctx)][n_seg][k] for occx_topk_merge.  The workspace
- * ends in a scheduler block (the record scorer's per-CTA tile counters,
- * a multiple of 256 bytes): it must be zero before the first call, and
- * every call leaves it zero.                                             */
+ * ends in a scheduler block (the record scorer's per-CTA tile counters
+ * and grid-wide per-segment bounds, a multiple of 256 bytes): it must be
+ * zero before the first call, and every call leaves it zero.             */
 int occx_score_workspace_bytes(const occx_ctx* ctx, uint32_t n_seg, uint32_t k,
                                uint64_t* bytes);
 int occx_score_lists(const occx_ctx* ctx);
-/* Zero the scheduler block at the end of a workspace of ws_bytes (once,
+/* Zero the scheduler block of a workspace sized for (n_seg, k) (once,
  * before the first occx_score_topk call on it; cudaMemsetAsync).        */
-int occx_score_workspace_init(const occx_ctx* ctx, void* d_ws, uint64_t ws_bytes, void* stream);
+int occx_score_workspace_init(const occx_ctx* ctx, void* d_ws, uint32_t n_seg, uint32_t k,
+                              void* stream);
 int occx_score_topk(const occx_ctx* ctx, const occx_arch_t* h_archs, int n_arch,
                     const occx_cand_t* d_cand, uint64_t n, uint64_t index_base,
                     int mode, const occx_vent_t* d_vtab, uint32_t n_var,

@@ -678,7 +678,7 @@ class ScorePlan:
         self.d_sum, self.d_feat, self.d_vtab, self.d_ws = (_DevPtr(base + o) for o in offs[1:])
         # the workspace's scheduler block starts zeroed (the scorer leaves it zero)
         _lib.check(_lib.load().occx_score_workspace_init(
-            self._ctx, _lib.ptr(self.d_ws), self.ws_bytes, _lib.stream_ptr()),
+            self._ctx, _lib.ptr(self.d_ws), self.n_seg, k, _lib.stream_ptr()),
             "occx_score_workspace_init")
         # K1 on device, then the feature table
         cols = [int(a["cost_key"]) for a in self.h_archs]

@@ -96,6 +96,7 @@ struct ScoreParams {
   uint64_t* partials;       // [gridDim.x][n_seg][k]
   uint32_t* sched;          // TMA feed: taken[gridDim.x], CTAs done; zero on entry and exit
   uint32_t steal;           // TMA feed: idle CTAs take tiles of the busiest chunk
+  unsigned long long* gthr; // TMA feed: grid-wide per-segment bound [n_seg]; zero on entry/exit
 };
 
 // Descending bitonic sort of one u64 per lane across the warp (lane 0 = largest).
@@ -147,6 +148,18 @@ __device__ __forceinline__ uint64_t list_merge_batch(uint64_t list, uint64_t x, 
 __device__ __forceinline__ void thr_raise(volatile uint64_t* s_thr, uint32_t seg, uint64_t v) {
   atomicMax(reinterpret_cast<unsigned long long*>(const_cast<uint64_t*>(s_thr + seg)),
             (unsigned long long)v);
+}
+
+// A warp whose full list's k-th key rose: raise the CTA bound; with a
+// grid-wide bound (TMA feed) also raise that, and pull a higher grid value
+// back into the CTA bound (the CTA's filters then use it).
+__device__ __forceinline__ void share_bound(volatile uint64_t* s_thr, unsigned long long* g_thr,
+                                            uint32_t seg, uint64_t v) {
+  thr_raise(s_thr, seg, v);
+  if (g_thr) {
+    const unsigned long long old = atomicMax(g_thr + seg, (unsigned long long)v);
+    if (old > v) thr_raise(s_thr, seg, old);
+  }
 }
 
 __device__ __forceinline__ void cta_insert(unsigned pend, uint64_t key, uint32_t seg,
@@ -226,7 +239,8 @@ __device__ __forceinline__ void wl_flush(WarpList& w, int lane, uint32_t k, vola
 
 __device__ __forceinline__ void wl_offer(uint64_t key, uint32_t seg, WarpList& w, int lane,
                                          uint32_t k, volatile uint64_t* s_thr,
-                                         volatile uint64_t* s_list, int* s_lock) {
+                                         volatile uint64_t* s_list, int* s_lock,
+                                         unsigned long long* g_thr = nullptr) {
   const bool mine = seg == w.seg;
   unsigned pend = __ballot_sync(0xffffffffu, !mine || key > w.thr);   // key 0 carries w.seg
   if (pend == 0) return;
@@ -253,7 +267,7 @@ __device__ __forceinline__ void wl_offer(uint64_t key, uint32_t seg, WarpList& w
     K2_COUNT(1);
     w.v = list_merge_batch(w.v, (pend >> lane) & 1u ? key : 0ull, lane, k);
     w.thr = warp_list_min(w.v, (int)k);
-    if (lane == 0 && w.thr > s_thr[w.seg]) thr_raise(s_thr, w.seg, w.thr);   // share the bound
+    if (lane == 0 && w.thr > s_thr[w.seg]) share_bound(s_thr, g_thr, w.seg, w.thr);
     return;
   }
   const uint64_t before = w.thr;
@@ -266,7 +280,8 @@ __device__ __forceinline__ void wl_offer(uint64_t key, uint32_t seg, WarpList& w
       w.thr = warp_list_min(w.v, (int)k);
     }
   }
-  if (lane == 0 && w.thr != before && w.thr > s_thr[w.seg]) thr_raise(s_thr, w.seg, w.thr);
+  if (lane == 0 && w.thr != before && w.thr > s_thr[w.seg])
+    share_bound(s_thr, g_thr, w.seg, w.thr);
 }
 
 // Shared-memory carve-up common to both feeds (after an optional TMA ring).
@@ -363,7 +378,9 @@ __device__ inline void k2_flush(const ScoreParams& p, const K2Shared& s) {
 template <int MODE, bool VT_SMEM>
 __device__ __forceinline__ void k2_process4(const K2Shared& s, K2Cache& cc, WarpList& wl,
                                             const uint4 (&r)[4], const uint64_t inv, int lane,
-                                            uint32_t k, bool exact = false) {
+                                            uint32_t k, bool exact = false,
+                                            unsigned long long* g_thr = nullptr,
+                                            uint32_t g_hi = 0) {
   uint64_t key[4];
   uint32_t seg[4];
   const bool hit = k2_hit(cc, r[0]) & k2_hit(cc, r[1]) & k2_hit(cc, r[2]) & k2_hit(cc, r[3]);
@@ -387,18 +404,23 @@ __device__ __forceinline__ void k2_process4(const K2Shared& s, K2Cache& cc, Warp
   // (lower-index) batch of this warp's forward walk, so a key whose high
   // word equals the list threshold's has a smaller inverse index and is
   // below it.  Once the walk has stepped back (a stolen tile: `exact`) the
-  // full keys are compared.  wl_offer compares the full keys either way.
+  // full keys are compared.  g_hi: the high word of the CTA / grid bound of
+  // the warp's segment (some warp's full list holds k keys at or above it,
+  // so a key not above it cannot make the top k; ">=" on high words since
+  // its index bits are foreign).  wl_offer compares the full keys.
   bool any = false;
   if (exact) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      any = any | (((uint32_t)(key[j] >> 32) != 0u) & ((seg[j] != wl.seg) | (key[j] > wl.thr)));
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t h = (uint32_t)(key[j] >> 32);
+      any = any | ((h != 0u) & ((seg[j] != wl.seg) | ((key[j] > wl.thr) & (h >= g_hi))));
+    }
   } else {
     const uint32_t thr_hi = (uint32_t)(wl.thr >> 32);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const uint32_t h = (uint32_t)(key[j] >> 32);
-      any = any | ((h != 0u) & ((seg[j] != wl.seg) | (h > thr_hi)));
+      any = any | ((h != 0u) & ((seg[j] != wl.seg) | ((h > thr_hi) & (h >= g_hi))));
     }
   }
   if (__any_sync(0xffffffffu, any)) {
@@ -407,7 +429,7 @@ __device__ __forceinline__ void k2_process4(const K2Shared& s, K2Cache& cc, Warp
 #endif
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      wl_offer(key[j], key[j] ? seg[j] : wl.seg, wl, lane, k, s.thr, s.list, s.lock);
+      wl_offer(key[j], key[j] ? seg[j] : wl.seg, wl, lane, k, s.thr, s.list, s.lock, g_thr);
 #ifdef OCCX_K2_TIMING
     K2_ADD(6, k2_clk() - c0);
 #endif
@@ -1202,6 +1224,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
     cc.x = cc.z = cc.w = 0xffffffffu;
     k2_fill<VT_SMEM>(s.c, make_uint4(0xffffffffu, 0, 0, 0xffffffffu), cc);
     bool stepped_back = false;         // a stolen tile came: exact list filter from then on
+    // grid-wide bound of the warp's segment, read one tile ahead (L2 latency)
+
     for (uint32_t t = 0;; ++t) {
       const uint32_t st = t % kTmaStages;
 #ifdef OCCX_K2_TIMING
@@ -1215,6 +1239,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
       if (tagged == kTileEnd) break;
       const uint32_t tile = tagged & ~kTileStolen;
       stepped_back |= (tagged & kTileStolen) != 0;
+      // the CTA bound of the warp's segment (it absorbs the grid-wide bound
+      // whenever a warp of this CTA raises it: share_bound)
+      const uint32_t cta_hi = wl.seg != kNoSeg ? (uint32_t)(s.thr[wl.seg] >> 32) : 0u;
       const uint64_t tb = (uint64_t)tile * kTmaTile;
       const uint32_t cnt = (uint32_t)min((uint64_t)kTmaTile, p.n - tb);
       const uint4* ring_tile = ring + (size_t)st * kTmaTile;
@@ -1253,7 +1280,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
 #pragma unroll
       for (int h = 0; h < kTmaSlices; ++h)
         k2_process4<MODE, VT_SMEM>(s, cc, wl, r[h], kIdxMask - p.index_base - tb - slice - 128u * h,
-                                   lane, p.k, stepped_back);
+                                   lane, p.k, stepped_back, p.gthr, cta_hi);
 #endif
 #ifdef OCCX_K2_TIMING
       if (lane == 0)
@@ -1272,8 +1299,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) score_topk_tma_kernel(const __
   if (threadIdx.x == 0) {
     // every producer of the grid has finished taking tiles once all CTAs
     // have counted themselves here: the last one resets the scheduler
-    if (atomicAdd(p.sched + gridDim.x, 1u) == gridDim.x - 1)
+    if (atomicAdd(p.sched + gridDim.x, 1u) == gridDim.x - 1) {
       for (uint32_t v = 0; v <= gridDim.x; ++v) p.sched[v] = 0;
+      for (uint32_t v = 0; v < p.n_seg; ++v) p.gthr[v] = 0;
+    }
   }
 #ifdef OCCX_K2_TIMING
   __syncthreads();
@@ -1599,25 +1628,28 @@ static int score_grid(const occx_ctx* ctx) {
 // Workspace: [score_grid][n_seg][k] per-CTA tables, then a 256-byte
 // scheduler block (TMA feed tile counter); zero before the first call,
 // every call leaves it zero.
-static uint64_t sched_bytes(const occx_ctx* ctx) {      // taken[grid] + done, 256-B units
+// taken[grid] + done, then the grid-wide per-segment bounds gthr[n_seg]; 256-B units
+static uint64_t sched_words_bytes(const occx_ctx* ctx) {
   return ((uint64_t)(score_grid(ctx) + 1) * 4 + 255) / 256 * 256;
+}
+static uint64_t sched_bytes(const occx_ctx* ctx, uint32_t n_seg) {
+  return sched_words_bytes(ctx) + ((uint64_t)n_seg * 8 + 255) / 256 * 256;
 }
 
 extern "C" int occx_score_workspace_bytes(const occx_ctx* ctx, uint32_t n_seg, uint32_t k,
                                           uint64_t* bytes) {
   if (!ctx || !bytes || k == 0 || k > OCCX_MAX_K || n_seg == 0) return OCCX_ERR_VALUE;
-  *bytes = (uint64_t)score_grid(ctx) * n_seg * k * 8 + sched_bytes(ctx);
+  *bytes = (uint64_t)score_grid(ctx) * n_seg * k * 8 + sched_bytes(ctx, n_seg);
   return OCCX_OK;
 }
 
 extern "C" int occx_score_lists(const occx_ctx* ctx) { return ctx ? score_grid(ctx) : 0; }
 
-extern "C" int occx_score_workspace_init(const occx_ctx* ctx, void* d_ws, uint64_t ws_bytes,
-                                         void* stream) {
-  if (!ctx || !d_ws) return OCCX_ERR_VALUE;
-  const uint64_t sb = sched_bytes(ctx);
-  if (ws_bytes < sb) return OCCX_ERR_VALUE;
-  OCCX_CUDA_TRY(cudaMemsetAsync(static_cast<char*>(d_ws) + (ws_bytes - sb), 0, sb,
+extern "C" int occx_score_workspace_init(const occx_ctx* ctx, void* d_ws, uint32_t n_seg,
+                                         uint32_t k, void* stream) {
+  if (!ctx || !d_ws || k == 0 || k > OCCX_MAX_K || n_seg == 0) return OCCX_ERR_VALUE;
+  const uint64_t tables = (uint64_t)score_grid(ctx) * n_seg * k * 8;
+  OCCX_CUDA_TRY(cudaMemsetAsync(static_cast<char*>(d_ws) + tables, 0, sched_bytes(ctx, n_seg),
                                 reinterpret_cast<cudaStream_t>(stream)));
   return OCCX_OK;
 }
@@ -1658,7 +1690,9 @@ extern "C" int occx_score_topk(const occx_ctx* ctx, const occx_arch_t* h_archs, 
   p.partials = static_cast<uint64_t*>(d_ws);
   const int grid = score_grid(ctx);
   const int feed = score_feed(ctx);
-  p.sched = reinterpret_cast<uint32_t*>(static_cast<char*>(d_ws) + need - sched_bytes(ctx));
+  p.sched = reinterpret_cast<uint32_t*>(static_cast<char*>(d_ws) + need - sched_bytes(ctx, n_seg));
+  p.gthr = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(p.sched) +
+                                                 sched_words_bytes(ctx));
   p.steal = (ctx->options & OCCX_CTX_K2_NO_STEAL) ? 0u : 1u;
   p.vt_smem = ((uint64_t)n_var * n_arch <= (uint64_t)kVtSmemMax) ? 1u : 0u;
   size_t smem = k2_tail_bytes(p.archs, n_var, n_seg, k, p.vt_smem != 0);

@@ -151,10 +151,10 @@ def test_workspace_scheduler_block_and_one_call_errors(env):
     from paper_1701_08547_b200.batch import _SpacePack
     torch, L, lib, plan, rec = env
     ctx = L.ctx()
-    assert lib.occx_score_workspace_init(ctx, None, plan.ws_bytes, L.stream_ptr()) == 1
-    assert lib.occx_score_workspace_init(ctx, L.ptr(plan.d_ws), 16, L.stream_ptr()) == 1
+    assert lib.occx_score_workspace_init(ctx, None, plan.n_seg, plan.k, L.stream_ptr()) == 1
+    assert lib.occx_score_workspace_init(ctx, L.ptr(plan.d_ws), plan.n_seg, 0, L.stream_ptr()) == 1
     ws = torch.full((plan.ws_bytes,), 0x5A, dtype=torch.uint8, device="cuda")
-    assert lib.occx_score_workspace_init(ctx, L.ptr(ws), plan.ws_bytes, L.stream_ptr()) == 0
+    assert lib.occx_score_workspace_init(ctx, L.ptr(ws), plan.n_seg, plan.k, L.stream_ptr()) == 0
     lists = plan.grid_lists * plan.n_seg * plan.k * 8
     assert int(ws[lists:].sum()) == 0 and int(ws[:lists].min()) == 0x5A
     out = torch.empty((plan.n_seg, plan.k), dtype=torch.int64, device="cuda")
