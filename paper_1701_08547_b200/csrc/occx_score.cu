@@ -840,7 +840,7 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
         const uint64_t inv = inv0 - (uint64_t)j;
         const uint64_t key = (v[j] & 0x1fc00000u)
             ? (((uint64_t)(v[j] | sb.hi | (uint32_t)(inv >> 32)) << 32) | (uint32_t)inv) : 0ull;
-        wl_offer(key, key ? sb.seg : wl.seg, wl, lane, p.k, s.thr, s.list, s.lock);
+        wl_offer(key, key ? sb.seg : wl.seg, wl, lane, p.k, s.thr, s.list, s.lock, p.gthr);
       }
     }
     o += 128;
@@ -882,7 +882,7 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
         const uint64_t inv = inv0 - (uint64_t)j;
         const uint64_t key = (v[j] & 0x1fc00000u)
             ? (((uint64_t)(v[j] | sb.hi | (uint32_t)(inv >> 32)) << 32) | (uint32_t)inv) : 0ull;
-        wl_offer(key, key ? sb.seg : wl.seg, wl, lane, p.k, s.thr, s.list, s.lock);
+        wl_offer(key, key ? sb.seg : wl.seg, wl, lane, p.k, s.thr, s.list, s.lock, p.gthr);
       }
     }
   };
@@ -916,7 +916,7 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
         const uint64_t inv = inv0 - (uint64_t)j;
         const uint64_t key = (v[j] & 0x1fc00000u)
             ? (((uint64_t)(v[j] | sb.hi | (uint32_t)(inv >> 32)) << 32) | (uint32_t)inv) : 0ull;
-        wl_offer(key, key ? sb.seg : wl.seg, wl, lane, p.k, s.thr, s.list, s.lock);
+        wl_offer(key, key ? sb.seg : wl.seg, wl, lane, p.k, s.thr, s.list, s.lock, p.gthr);
       }
     }
   };
@@ -989,13 +989,21 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
         r[j] = g < we ? ig_record(ic, pool, g) : make_uint4(0, 0, 0, 0xffffffffu);
       }
     }
-    k2_process4<MODE, VT_SMEM>(s, cc, wl, r, kIdxMask - q.key_off - g0, lane, p.k);
+    k2_process4<MODE, VT_SMEM>(s, cc, wl, r, kIdxMask - q.key_off - g0, lane, p.k, false, p.gthr,
+                               wl.seg != kNoSeg ? (uint32_t)(s.thr[wl.seg] >> 32) : 0u);
   }
   k2_stage(wl, lane, p.k, stage, threadIdx.x >> 5, kIgWarps);
   __syncthreads();
   if (threadIdx.x < 32) k2_merge_staged(stage, 2 * kIgWarps, p.k, s.thr, s.list, s.lock);
   __syncthreads();
   k2_flush(p, s);
+  if (threadIdx.x == 0) {           // the last CTA returns the grid bounds to zero
+    __threadfence();
+    if (atomicAdd(p.sched + gridDim.x, 1u) == gridDim.x - 1) {
+      for (uint32_t v = 0; v < p.n_seg; ++v) p.gthr[v] = 0;
+      p.sched[gridDim.x] = 0;
+    }
+  }
 }
 
 // ---- TMA feed ---------------------------------------------------------------
@@ -1850,7 +1858,10 @@ extern "C" int occx_score_space_host(const occx_ctx* ctx, const occx_arch_t* h_a
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   char* base = static_cast<char*>(d_buf);
   OCCX_CUDA_TRY(cudaMemcpyAsync(base, h_blob, blob_bytes, cudaMemcpyHostToDevice, s));
-  // the record scorer's scheduler block stays zero (this path uses K2i only)
+  // the workspace's scheduler block (done counter, grid-wide segment bounds)
+  // starts zeroed; the scorer leaves it zero
+  OCCX_CUDA_TRY(cudaMemsetAsync(base + b.ws + (b.ws_bytes - sched_bytes(ctx, n_seg)), 0,
+                                sched_bytes(ctx, n_seg), s));
   int32_t cols[kMaxArchs];
   for (int i = 0; i < n_arch; ++i) cols[i] = h_archs[i].cost_key;
   auto at = [&](int i) { return base + blob_off[i]; };
@@ -1918,6 +1929,12 @@ extern "C" int occx_score_space(const occx_ctx* ctx, const occx_arch_t* h_archs,
   q.sp.n_seg = n_seg;
   q.sp.k = k;
   q.sp.partials = static_cast<uint64_t*>(d_ws);
+  // scheduler block: the done counter (after grid tables' worth of words) and
+  // the grid-wide per-segment bounds, as for the record scorer
+  q.sp.sched = reinterpret_cast<uint32_t*>(static_cast<char*>(d_ws) + need -
+                                           sched_bytes(ctx, n_seg));
+  q.sp.gthr = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(q.sp.sched) +
+                                                    sched_words_bytes(ctx));
   q.desc = d_desc;
   q.pool = d_pool;
   q.n_desc = n_desc;
