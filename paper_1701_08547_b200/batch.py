@@ -166,7 +166,7 @@ def pack_launches(launches, arch_index=None) -> np.ndarray:
 def occupancy_records(archs, d_records, n: int, mode: Mode = Mode.CORRECTED, d_out=None):
     """Device-level Kd: records already in HBM -> occx_occ_t array (device)."""
     torch = _torch()
-    h_archs = pack_archs(_arch_list(archs))
+    h_archs = _packed_archs(tuple(_arch_list(archs)))
     out = d_out if d_out is not None else _empty(n * _lib.OCC.itemsize)
     _lib.check(_lib.load().occx_occupancy_batch(
         _lib.ctx(), _lib.ptr(h_archs), len(h_archs), _lib.ptr(d_records), n,
@@ -211,7 +211,7 @@ def suggest_batch(requests, mode: Mode = Mode.CORRECTED,
         inp[i] = (index[id(arch)], min(regs, U32_MAX), min(smem, U32_MAX), 0)
     if not requests:
         return []
-    h_archs = pack_archs(archs)
+    h_archs = _packed_archs(tuple(archs))
     d_in = _to_device(inp)
     d_out = _empty(len(inp) * _lib.SUGG.itemsize)
     _lib.check(_lib.load().occx_suggest_batch(
