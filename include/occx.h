@@ -262,6 +262,9 @@ int occx_build_vtab(const occx_ctx* ctx, const occx_mixsum_t* d_sum,
 int occx_score_workspace_bytes(const occx_ctx* ctx, uint32_t n_seg, uint32_t k,
                                uint64_t* bytes);
 int occx_score_lists(const occx_ctx* ctx);
+/* cudaStreamSynchronize(stream) (the scalar API's one-launch path waits on
+ * results the kernel wrote into pinned host memory).                     */
+int occx_stream_sync(void* stream);
 /* Zero the scheduler block of a workspace sized for (n_seg, k) (once,
  * before the first occx_score_topk call on it; cudaMemsetAsync).        */
 int occx_score_workspace_init(const occx_ctx* ctx, void* d_ws, uint32_t n_seg, uint32_t k,

@@ -67,6 +67,7 @@ SIGNATURES = {
     "occx_build_vtab": ([_P, _P, _P, _U32, _U32, _P, _P, _P, _P], _I),
     "occx_score_workspace_bytes": ([_P, _U32, _U32, _P], _I),
     "occx_score_lists": ([_P], _I),
+    "occx_stream_sync": ([_P], _I),
     "occx_score_workspace_init": ([_P, _P, _U32, _U32, _P], _I),
     "occx_space_buf_bytes": ([_P, _U64, _U32, _U32, _U32, _U32, _P, _P], _I),
     "occx_score_space_host": ([_P, _P, _I, _P, _U64, _P, _U32, _U32, _U32, _P, _D, _I, _U64,

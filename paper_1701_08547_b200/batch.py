@@ -16,9 +16,11 @@ from __future__ import annotations
 import bisect
 import ctypes
 import functools
+import struct
 import sys
+import threading
 from dataclasses import dataclass, field
-from typing import Sequence
+from typing import NamedTuple, Sequence
 
 import numpy as np
 from itertools import chain
@@ -175,6 +177,81 @@ def occupancy_records(archs, d_records, n: int, mode: Mode = Mode.CORRECTED, d_o
     return out
 
 
+class _Lane(threading.local):
+    """Per-thread page of pinned host memory the device reads and writes
+    directly (UVA): the scalar API's one-launch path, no device buffers and
+    no copies.  Allocated once per thread."""
+
+    page = None
+
+
+_LANE = _Lane()
+
+
+def _lane():
+    if _LANE.page is None:
+        torch = _torch()
+        t = torch.zeros(4096, dtype=torch.uint8, pin_memory=True)
+        _LANE.page = (t, t.numpy(), t.data_ptr())
+    return _LANE.page
+
+
+def _sync(stream=None) -> None:
+    _lib.check(_lib.load().occx_stream_sync(_lib.stream_ptr(stream)), "occx_stream_sync")
+
+
+# occx_cand_t / occx_occ_t as struct layouts for the one-launch path
+_REC1 = struct.Struct("<IIHHHBB")       # variant, smem, threads, blocks, regs, arch, aux
+_OCC1 = struct.Struct("<8B4Id")         # wpb, lw, blocks, aw, limiter, status, -, -,
+                                        # limit_regs, limit_smem, reg_warp_limit, -, occupancy
+
+
+class OccRow(NamedTuple):
+    """One occx_occ_t, unpacked (the scalar API's result row)."""
+
+    warps_per_block: int
+    limit_warps: int
+    active_blocks: int
+    active_warps: int
+    limiter: int
+    status: int
+    limit_regs: int
+    limit_smem: int
+    reg_warp_limit: int
+    occupancy: float
+
+    def result(self, mode: Mode) -> OccupancyResult:
+        if self.status == 2:
+            raise IllegalLaunchError("threads_per_block outside the architecture's range")
+        if self.status:
+            raise ValueError("invalid candidate record")
+        return OccupancyResult(
+            warps_per_block=self.warps_per_block, limit_warps=self.limit_warps,
+            limit_regs=self.limit_regs, limit_smem=self.limit_smem,
+            active_blocks=self.active_blocks, active_warps=self.active_warps,
+            occupancy=self.occupancy, limiter=LIMITER_OF_CODE[self.limiter], mode=mode)
+
+
+def occupancy_single(arch, threads: int, regs: int, smem: int,
+                     mode: Mode = Mode.CORRECTED) -> OccRow:
+    """occupancy() of one launch: the record and the result live in pinned
+    host memory the kernel reads and writes over UVA -- one launch and one
+    stream synchronize (ref occupancy.py:163-195).  Same clamps as
+    pack_launches."""
+    if threads < 0 or regs < 0 or smem < 0:
+        raise IllegalLaunchError("resource amounts must be non-negative")
+    _, page, base = _lane()
+    _REC1.pack_into(page, 0, 0, min(smem, U32_MAX), min(threads, 0xFFFF), 0,
+                    min(regs, 0xFFFF), 0, 0)
+    h_archs = _packed_archs((arch,))
+    _lib.check(_lib.load().occx_occupancy_batch(
+        _lib.ctx(), h_archs.ctypes.data, 1, base, 1, MODE_CODE[Mode(mode)], base + 256,
+        _lib.stream_ptr()), "occx_occupancy_batch")
+    _sync()
+    v = _OCC1.unpack_from(page, 256)
+    return OccRow(v[0], v[1], v[2], v[3], v[4], v[5], v[8], v[9], v[10], v[12])
+
+
 def occupancy_batch(archs, launches, mode: Mode = Mode.CORRECTED, arch_index=None) -> OccBatch:
     """occupancy() for many launches on the GPU (ref occupancy.py:163-195)."""
     mode = Mode(mode)
@@ -212,12 +289,21 @@ def suggest_batch(requests, mode: Mode = Mode.CORRECTED,
     if not requests:
         return []
     h_archs = _packed_archs(tuple(archs))
-    d_in = _to_device(inp)
-    d_out = _empty(len(inp) * _lib.SUGG.itemsize)
+    if len(inp) == 1:                  # the scalar API: one launch on the lane page
+        _, page, base = _lane()
+        page[:inp.nbytes] = inp.view(np.uint8)
+        d_in, d_out = _DevPtr(base), _DevPtr(base + 256)
+    else:
+        d_in = _to_device(inp)
+        d_out = _empty(len(inp) * _lib.SUGG.itemsize)
     _lib.check(_lib.load().occx_suggest_batch(
         _lib.ctx(), _lib.ptr(h_archs), len(h_archs), _lib.ptr(d_in), len(inp),
         MODE_CODE[mode], _lib.ptr(d_out), _lib.stream_ptr()), "occx_suggest_batch")
-    out = _to_host(d_out, _lib.SUGG, len(inp))
+    if len(inp) == 1:
+        _sync()
+        out = page[256:256 + _lib.SUGG.itemsize].view(_lib.SUGG).copy()
+    else:
+        out = _to_host(d_out, _lib.SUGG, len(inp))
     reports = []
     for i, req in enumerate(requests):
         arch, res = req[0], req[1]
@@ -438,8 +524,9 @@ class FeatureBatch:
         return [float(x) for x in self.sums["intensity"]]
 
     def one(self, m: int, j: int, need_cost: bool = True) -> Features:
-        f = self.feat[m * self.n_col + j]
-        st = int(f["status"])
+        # one C-level conversion of the row: (cost, coef, cycles, shares,
+        # per_class, status, pc_status)
+        cost, coef, cyc, shares, pcl, st, pc_st = self.feat[m * self.n_col + j].tolist()
         cc = self.ccs[j]
         if st == 3:
             from .mix import sm_key
@@ -450,19 +537,16 @@ class FeatureBatch:
             _lib.check(st, "occx_feature_score")
         mix = self.mixes[m]
         per_class = None
-        if int(f["pc_status"]) == 0:
+        if pc_st == 0:
             per_class = {}
-            for cls in mix.counts:
-                if cls is not OpClass.UNCLASSIFIED and mix.counts[cls]:
-                    per_class[cls] = float(f["per_class"][CPI_ROW[cls]])
+            for cls, n in mix.counts.items():
+                if cls is not OpClass.UNCLASSIFIED and n:
+                    per_class[cls] = pcl[CPI_ROW[cls]]
             if mix.reg_operands:
-                per_class[OpClass.REGS] = float(f["per_class"][CPI_ROW[OpClass.REGS]])
-        return Features(
-            cost=float(f["cost"]),
-            coefficients={c: float(f["coef"][i]) for i, c in enumerate(_CATS)},
-            cycles={c: float(f["cycles"][i]) for i, c in enumerate(_CATS)},
-            shares={c: float(f["shares"][i]) for i, c in enumerate(_CATS)},
-            per_class_map=per_class)
+                per_class[OpClass.REGS] = pcl[CPI_ROW[OpClass.REGS]]
+        return Features(cost=cost, coefficients=dict(zip(_CATS, coef)),
+                        cycles=dict(zip(_CATS, cyc)), shares=dict(zip(_CATS, shares)),
+                        per_class_map=per_class)
 
 
 def feature_records(d_mix, n_mix: int, cols: Sequence[int], cpi: np.ndarray, scale: float,
@@ -481,6 +565,26 @@ def feature_records(d_mix, n_mix: int, cols: Sequence[int], cpi: np.ndarray, sca
     return d_sum, d_feat
 
 
+_MIX1 = struct.Struct("<32IQII")        # occx_mix_t: counts[16] first_key[16] regs n_instr rsv
+
+
+def _pack_mix_into(page, mix) -> None:
+    """One InstructionMix as occx_mix_t at the start of `page` (pack_mixes
+    for a single mix, without numpy)."""
+    w = [0] * 16 + [U32_MAX] * 16
+    total = 0
+    for rank, (cls, c) in enumerate(mix.counts.items()):
+        if c > U32_MAX:
+            raise DeviceError("per-class count above 2^32-1")
+        d = DEVICE_ID[cls]
+        w[d] = c
+        w[16 + d] = rank
+        total += c
+    if mix.reg_operands >= 1 << 64:
+        raise DeviceError("reg_operands above 2^64-1")
+    _MIX1.pack_into(page, 0, *w, mix.reg_operands, min(total, U32_MAX), 0)
+
+
 def feature_score(mixes, ccs, scale: float = 1.0,
                   table: ThroughputTable = DEFAULT_THROUGHPUT,
                   sum_mode: int = SUM_MODE) -> FeatureBatch:
@@ -488,6 +592,16 @@ def feature_score(mixes, ccs, scale: float = 1.0,
     mixes = list(mixes)
     ccs = list(ccs)
     cols = [cost_key_of_cc(cc) for cc in ccs]
+    if len(mixes) == 1 and len(cols) <= 1:       # the scalar API: one launch on the lane page
+        _, page, base = _lane()
+        _pack_mix_into(page, mixes[0])
+        feature_records(_DevPtr(base), 1, cols, table.cpi_matrix(), scale, sum_mode,
+                        d_sum=_DevPtr(base + 256), d_feat=_DevPtr(base + 512))
+        _sync()
+        sums = page[256:256 + _lib.MIXSUM.itemsize].view(_lib.MIXSUM).copy()
+        feat = (page[512:512 + _lib.FEAT.itemsize].view(_lib.FEAT).copy() if cols
+                else np.zeros(0, _lib.FEAT))
+        return FeatureBatch(sums, feat, len(cols), mixes, ccs)
     pm = pack_mixes(mixes)
     d_sum, d_feat = feature_records(_to_device(pm), len(mixes), cols, table.cpi_matrix(),
                                     scale, sum_mode)

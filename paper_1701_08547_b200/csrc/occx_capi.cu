@@ -24,6 +24,11 @@ extern "C" const char* occx_status_string(int status) {
   }
 }
 
+extern "C" int occx_stream_sync(void* stream) {
+  OCCX_CUDA_TRY(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
+  return OCCX_OK;
+}
+
 extern "C" int occx_ctx_create(int device, occx_ctx** out) {
   return occx_ctx_create_ex(device, 0u, out);
 }

@@ -100,8 +100,8 @@ def _thread_candidates(ws: int, wmp: int, bmp: int, tmax: int) -> tuple[int, ...
 
 
 def _one(arch, threads, regs, smem, mode):
-    from .batch import occupancy_batch
-    return occupancy_batch(arch, [(threads, regs, smem)], mode)
+    from .batch import occupancy_single
+    return occupancy_single(arch, threads, regs, smem, mode)
 
 
 def _checked(arch, threads):
@@ -120,26 +120,25 @@ def warps_per_block(arch: ArchSpec, threads: int) -> int:
 def limit_by_warps(arch: ArchSpec, threads: int) -> int:
     """ref occupancy.py:104-108."""
     _checked(arch, threads)
-    return int(_one(arch, threads, 0, 0, Mode.CORRECTED).limit_warps[0])
+    return _one(arch, threads, 0, 0, Mode.CORRECTED).limit_warps
 
 
 def register_warp_limit(arch: ArchSpec, regs_per_thread: int) -> int:
     """ref occupancy.py:111-124."""
-    return int(_one(arch, arch.warp_size, regs_per_thread, 0,
-                    Mode.CORRECTED).reg_warp_limit[0])
+    return _one(arch, arch.warp_size, regs_per_thread, 0, Mode.CORRECTED).reg_warp_limit
 
 
 def limit_by_registers(arch: ArchSpec, threads: int, regs_per_thread: int,
                        mode: Mode = Mode.CORRECTED) -> int:
     """ref occupancy.py:127-145."""
     _checked(arch, threads)
-    return int(_one(arch, threads, regs_per_thread, 0, mode).limit_regs[0])
+    return _one(arch, threads, regs_per_thread, 0, mode).limit_regs
 
 
 def limit_by_smem(arch: ArchSpec, shared_per_block: int,
                   mode: Mode = Mode.CORRECTED) -> int:
     """ref occupancy.py:148-160 (no thread check, like the reference)."""
-    return int(_one(arch, arch.warp_size, 0, shared_per_block, mode).limit_smem[0])
+    return _one(arch, arch.warp_size, 0, shared_per_block, mode).limit_smem
 
 
 def occupancy(arch: ArchSpec, launch: LaunchInput,
@@ -149,7 +148,7 @@ def occupancy(arch: ArchSpec, launch: LaunchInput,
     _checked(arch, launch.threads_per_block)
     r = _one(arch, launch.threads_per_block, launch.regs_per_thread,
              launch.shared_per_block, mode)
-    return r.result(0)
+    return r.result(Mode(mode))
 
 
 def suggest(arch: ArchSpec, resources, mode: Mode = Mode.CORRECTED,
