@@ -474,8 +474,8 @@ def secondary_config3_e2e(n_kernels: int = 1000, reps: int = 5):
 
 def secondary_scalar_api(reps: int = 300):
     """The reference's scalar entry points called one at a time (a caller
-    looping over the drop-in API): every call is a batch of one -- pack, H2D,
-    one launch, D2H, synchronize -- with no CPU fallback.  Per-call latency
+    looping over the drop-in API): every call is one launch whose input and
+    output live in pinned host memory, then a synchronize -- no CPU fallback.  Per-call latency
     beside the reference's measured 5.27 us per occupancy() call (SURVEY
     §6, one core)."""
     import paper_1701_08547_b200 as P
@@ -495,7 +495,8 @@ def secondary_scalar_api(reps: int = 300):
         out[name] = {"us_per_call": (time.perf_counter() - t0) / reps * 1e6}
     out["reference_us_per_call"] = {"occupancy": 5.27, "cost_estimate": 12.2,
                                     "source": "SURVEY §6 / §8(a), one core, Python 3.12"}
-    out["note"] = ("a batch of one per call (H2D + launch + D2H + sync); the batch "
+    out["note"] = ("one launch per call on a per-thread page of pinned host memory the "
+                   "kernel reads and writes over UVA, then a stream synchronize; the batch "
                    "entry points are the intended use")
     return out
 
