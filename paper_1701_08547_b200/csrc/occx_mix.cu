@@ -32,10 +32,11 @@
 // they can overflow.
 // Dict insertion order (it decides the summation order of the FLOPS terms
 // in mix.py:278) is recovered as first_key[c] = min over occurrences of
-// 2*i (class of instruction i) or 2*i+1 (guard PredIns of instruction i);
-// a warp OR-reduction per piece finds classes not seen before in the
-// kernel and only then are their first positions located (one shared
-// atomicMin per (row, class) leader found with MATCH.ANY).
+// 2*i (class of instruction i) or 2*i+1 (guard PredIns of instruction i).
+// The streaming count does not track it: when a kernel is finished, its
+// counters name the classes present, and its records are re-read from the
+// start (L2 hits) in 32-position rows until each of them is located -- one
+// MATCH.ANY per row (first_keys()).
 #include "occx_common.cuh"
 
 using namespace occx;
@@ -112,90 +113,53 @@ __device__ __forceinline__ uint32_t seg_search(const uint64_t* off, uint32_t n, 
   return lo;
 }
 
-// One bit (the nibble's low bit) per non-zero 4-bit counter.
-__device__ __forceinline__ uint32_t nibble_presence(uint32_t v) {
-  const uint32_t t = v | (v >> 1);
-  return (t | (t >> 2)) & 0x11111111u;
-}
-
 // Per-warp state of the kernel being reduced.
 struct MixAcc {
   uint32_t be0, be1, bo0, bo1;     // byte counters: even / odd classes
-  uint32_t seen_lo, seen_hi;       // nibble presence so far in this kernel
   uint32_t regs, total;
   int pieces;
 };
 
-// Count one piece: lv[e] are the class-table values (byte offsets into the
-// increment table, kNullLv = not in this kernel); keybase + pic(e) is the
-// record's position in its kernel.
-__device__ __forceinline__ void count_piece(MixAcc& a, const uint32_t (&lv)[8],
-                                            const unsigned char* incb, uint32_t* my_first,
-                                            uint32_t keybase, int lane) {
-  uint32_t h0 = 0, h1 = 0, v0 = 0, v1 = 0;        // h: records of the first row block (u = 0)
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
+// Class records (the 15-entry identity class table, what the tokenizer
+// emits): the increment table is indexed directly by the record's low byte
+// (sig << 1 | guard), 256 entries + a zero (null) entry per lane, so a
+// record's increment address is ONE byte permute (low byte << 8 | lane * 8)
+// instead of mask + class-table LDS.U8 + shift.
+constexpr uint32_t kIdentEntries = 257;
+constexpr uint32_t kIdentNull = 256u << 8;
+__device__ __forceinline__ uint32_t ident_offset(uint32_t r, uint32_t lane8) {
+  return __byte_perm(r, lane8, 0x5504u);      // bytes: lane8.b0, r.b0, 0, 0
+}
+
+// A record's sixteen-nibble increment: lv is the lookup value -- a
+// class-table byte (byte offset / 64 into the increment table, kNullLv = not
+// in this kernel), or with kIdent the increment's byte offset itself
+// (kIdentNull + lane * 8 = not in this kernel).
+template <bool kIdent>
+__device__ __forceinline__ void increment(uint32_t l, int e, const unsigned char* incb,
+                                          uint32_t& dx, uint32_t& dy) {
+  if (kIdent) {
+    const uint2 d = *reinterpret_cast<const uint2*>(incb + l);
+    dx = d.x;
+    dy = d.y;
+  } else if (e < kLdsRecords) {    // shared increment table: entry at byte 2 * l
+    const uint2 d = *reinterpret_cast<const uint2*>(incb + (l << 6));   // entry l/4, this lane's copy
+    dx = d.x;
+    dy = d.y;
+  } else {                         // arithmetic: balances the shared-memory and ALU pipes
     // class nibble increment 1 << 4c as a 64-bit shift (shift >= 64, the
     // null entry, gives 0); a counted guard adds PredIns (nibble 11) and the
     // marker (nibble 15): bit 7 of the entry times 0x10001000 >> 7
-    const uint32_t l = lv[e];
-    uint32_t dx, dy;
-    if (e < kLdsRecords) {         // shared increment table: entry at byte 2 * l
-      const uint2 d = *reinterpret_cast<const uint2*>(incb + (l << 6));   // entry l/4, this lane's copy
-      dx = d.x;
-      dy = d.y;
-    } else {                       // arithmetic: balances the shared-memory and ALU pipes
-      asm("{\n\t.reg .b64 t;\n\tshl.b64 t, 1, %2;\n\tmov.b64 {%0, %1}, t;\n\t}"
-          : "=r"(dx), "=r"(dy) : "r"(l & 0x7fu));
-      dy += (l & 0x80u) * 0x200020u;
-    }
-    if (e < 4) {
-      h0 += dx;
-      h1 += dy;
-    } else {
-      v0 += dx;
-      v1 += dy;
-    }
+    asm("{\n\t.reg .b64 t;\n\tshl.b64 t, 1, %2;\n\tmov.b64 {%0, %1}, t;\n\t}"
+        : "=r"(dx), "=r"(dy) : "r"(l & 0x7fu));
+    dy += (l & 0x80u) * 0x200020u;
   }
-  v0 += h0;
-  v1 += h1;
-  // classes (nibbles) present in this lane's piece -> warp presence
-  const uint32_t pres_lo = __reduce_or_sync(0xffffffffu, nibble_presence(v0));
-  const uint32_t pres_hi = __reduce_or_sync(0xffffffffu, nibble_presence(v1));
-  const uint32_t new_lo = pres_lo & ~a.seen_lo, new_hi = pres_hi & ~a.seen_hi;
-  if (new_lo | new_hi) {                                   // a class new to this kernel
-    a.seen_lo |= pres_lo;
-    a.seen_hi |= pres_hi;
-    // Record e of every lane forms a row ordered by lane, so the first
-    // occurrence of a class in the row is its lowest lane: one leader per
-    // (row, class) does the shared atomicMin (no same-address serialisation).
-    // Rows 0-3 (u = 0) hold positions below rows 4-7; the second block is
-    // only searched when a new class is absent from the first.
-    uint32_t lt;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
-    const uint32_t first_lo = __reduce_or_sync(0xffffffffu, nibble_presence(h0));
-    const uint32_t first_hi = __reduce_or_sync(0xffffffffu, nibble_presence(h1));
-    // rows of block 0 only when a new class occurs there, of block 1 only
-    // when one is absent from block 0 (a piece may start or end mid-chunk);
-    // the guard rows only while no counted guard has been seen (nibble 15)
-    const int row0 = ((new_lo & first_lo) | (new_hi & first_hi)) ? 0 : 4;
-    const int rows = ((new_lo & ~first_lo) | (new_hi & ~first_hi)) ? 8 : 4;
-    const bool guard_new = (new_hi & 0x10000000u) != 0u;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      if (e >= rows) break;
-      if (e < row0) continue;
-      const uint32_t c = lv[e] >> 2 & 15u;
-      const uint32_t pos = keybase + 128u * (uint32_t)(e >> 2) + 4u * (uint32_t)lane + (uint32_t)(e & 3);
-      const uint32_t same = __match_any_sync(0xffffffffu, c);
-      if ((same & lt) == 0) atomicMin(my_first + c, 2u * pos);   // slot 15 (padding) is never read
-      // guard PredIns (non-CTRL class): key 2*pos + 1, tracked in slot 16
-      if (guard_new) {
-        const uint32_t gb = __ballot_sync(0xffffffffu, lv[e] & 128u);
-        if ((lv[e] & 128u) && (gb & lt) == 0) atomicMin(my_first + 16, 2u * pos + 1);
-      }
-    }
-  }
+}
+
+// Fold a piece's per-lane nibble sums (<= 8 records: no nibble overflows)
+// into the byte counters.
+__device__ __forceinline__ void add_piece(MixAcc& a, uint32_t v0, uint32_t v1, uint32_t* xch,
+                                          int lane) {
   a.be0 += v0 & 0x0f0f0f0fu;
   a.bo0 += (v0 >> 4) & 0x0f0f0f0fu;
   a.be1 += v1 & 0x0f0f0f0fu;
@@ -203,21 +167,97 @@ __device__ __forceinline__ void count_piece(MixAcc& a, const uint32_t (&lv)[8],
   if (++a.pieces == kFlushPieces) {
     a.pieces = 0;
     const uint32_t w[4] = {a.be0, a.be1, a.bo0, a.bo1};
-    reduce_counters_eo(w, lane, a.total, my_first + 24);
+    reduce_counters_eo(w, lane, a.total, xch);
     a.be0 = a.be1 = a.bo0 = a.bo1 = 0;
   }
 }
 
+// Count one piece.  Counting only: the first positions are found once per
+// kernel by first_keys().
+template <bool kIdent>
+__device__ __forceinline__ void count_piece(MixAcc& a, const uint32_t (&lv)[8],
+                                            const unsigned char* incb, uint32_t* xch, int lane) {
+  uint32_t v0 = 0, v1 = 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    uint32_t dx, dy;
+    increment<kIdent>(lv[e], e, incb, dx, dy);
+    v0 += dx;
+    v1 += dy;
+  }
+  add_piece(a, v0, v1, xch, lane);
+}
+
+// Dict insertion order (mix.py:256-259): first_key[c] = 2 * (position of the
+// first class-c record), and for PredIns the smaller of that and 2 * (first
+// counted guard) + 1.  The kernel's records are re-read from its start (L2
+// hits: the warp streamed them moments ago) in blocks of 128 positions,
+// lane l holding positions 4l..4l+3, until every class the counters saw is
+// located.  A lane's class mask (bit c, bit 15 = a counted guard) ORed
+// over the lower lanes (a 5-step shuffle scan) leaves, in the lane's own
+// mask, exactly the classes whose first occurrence in the block it holds.
+// `need` bits: classes 0-14 (bit 11 = class-11 records, i.e. nibble 11
+// minus the guards) and 15 = a counted guard.
+template <bool kIdent>
+__device__ __forceinline__ void first_keys(const uint32_t* kin, uint32_t n, uint32_t need,
+                                           const unsigned char* lut, uint32_t lut_mask,
+                                           const uint16_t* fbits, uint32_t* slot, int lane) {
+  for (uint32_t s = 4u * (uint32_t)lane; need; s += 128u) {
+    uint32_t bits[4], pres = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t pos = s + (uint32_t)j;
+      if (kIdent) {               // class records: the mask from the record's low byte
+        bits[j] = pos < n ? (uint32_t)fbits[__ldg(kin + pos) & 0xffu] : 0u;
+      } else {
+        const uint32_t lv = pos < n ? (uint32_t)lut[__ldg(kin + pos) & lut_mask] : kNullLv;
+        // bit c (class 15 = not counted, e.g. the null entry), bit 15 = a counted guard
+        bits[j] = ((1u << (lv >> 2 & 15u)) & 0x7fffu) | ((lv & 128u) << 8);
+      }
+      pres |= bits[j];
+    }
+    uint32_t incl = pres;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl |= y;
+    }
+    uint32_t excl = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) excl = 0;
+    uint32_t mine = pres & ~excl & need;
+    if (mine) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t hit = bits[j] & mine;
+        const uint32_t pos = s + (uint32_t)j;
+        if (hit & 0x7fffu) slot[__ffs(hit & 0x7fffu) - 1] = 2u * pos;
+        if (hit & 0x8000u) slot[15] = 2u * pos + 1u;
+        mine &= ~hit;
+      }
+    }
+    need &= ~__shfl_sync(0xffffffffu, incl, 31);
+  }
+  __syncwarp();
+}
+
+template <bool kIdent>
 __device__ __forceinline__ void finish_kernel(MixAcc& a, uint32_t* my_first, occx_mix_t* o,
-                                              uint32_t n_instr, int lane) {
+                                              const uint32_t* kin, uint32_t n_instr,
+                                              const unsigned char* lut, uint32_t lut_mask,
+                                              const uint16_t* fbits, int lane) {
   {
     const uint32_t w[4] = {a.be0, a.be1, a.bo0, a.bo1};
     reduce_counters_eo(w, lane, a.total, my_first + 24);
   }
-  uint32_t first = lane < 17 ? my_first[lane] : kAbsent;
-  const uint32_t gfirst = __shfl_sync(0xffffffffu, first, 16);
+  // lane c < 16 holds nibble c's total: class c's count (PredIns includes the
+  // counted guards), nibble 15 = counted guards
+  const uint32_t guards = __shfl_sync(0xffffffffu, a.total, 15);
+  const uint32_t own = lane == (int)kPred ? a.total - guards : a.total;
+  const uint32_t need = __ballot_sync(0xffffffffu, lane < 16 && own != 0u) & 0xffffu;
+  first_keys<kIdent>(kin, n_instr, need, lut, lut_mask, fbits, my_first, lane);
+  uint32_t first = (lane < 16 && ((need >> lane) & 1u)) ? my_first[lane] : kAbsent;
+  const uint32_t gfirst = __shfl_sync(0xffffffffu, first, 15);
   if (lane == (int)kPred && gfirst < first) first = gfirst;
-  if (lane < 17) my_first[lane] = kAbsent;               // reset for the warp's next kernel
   __syncwarp();
   // 64-bit total from two 16-bit-half warp sums (a lane's u32 cannot wrap:
   // kernels are < 2^29 records, <= 255 operands each, 1/32 of them per lane)
@@ -226,7 +266,7 @@ __device__ __forceinline__ void finish_kernel(MixAcc& a, uint32_t* my_first, occ
       ((uint64_t)__reduce_add_sync(0xffffffffu, a.regs >> 16) << 16);
   if (lane < 16) {
     o->counts[lane] = lane < 15 ? a.total : 0u;
-    o->first_key[lane] = (lane < 15 && a.total) ? first : kAbsent;
+    o->first_key[lane] = lane < 15 ? first : kAbsent;
   }
   if (lane == 0) {
     o->reg_operands = reg_total;
@@ -244,18 +284,139 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Shared-memory layout: [64] u64 increments | [warps][32] first positions
-// (slots 0-16) and reduction scratch (24-31) | per-warp ring of kDepth chunks (kChunk records each) | class table.
-constexpr int kFirstStride = 32;                      // per warp: 17 first slots, 8-word scratch at 24
-__host__ __device__ constexpr size_t mix_ring_offset() { return 64 * 32 * 8 + kWarps * kFirstStride * 4; }
+// Shared-memory layout: increments ([64][32] u64, or [257][32] when the
+// call may use class records) | [warps][32] first positions (slots 0-15)
+// and reduction scratch (24-31) | per-warp ring of kDepth chunks (kChunk
+// records each) | class table.
+constexpr int kFirstStride = 32;                      // per warp: 16 first slots, 8-word scratch at 24
+__host__ __device__ constexpr size_t mix_inc_bytes(bool may_ident) {
+  return may_ident ? kIdentEntries * 32u * 8u + 256u * 2u : 64u * 32u * 8u;   // + class masks
+}
+__host__ __device__ constexpr size_t mix_ring_offset(bool may_ident) {
+  return mix_inc_bytes(may_ident) + kWarps * kFirstStride * 4;
+}
 
-template <int kDepth>
+// The streaming loop over the warp's record range (see the file comment).
+struct MixRun {
+  const uint4* gsrc;          // vector 64c + 32u of the warp's chunk grid, this lane
+  uint4* my_ring;
+  uint32_t ring_s, re, kb, ks, ke;
+  uint64_t cs0;
+};
+
+template <bool kIdent, int kDepth>
+__device__ __forceinline__ void mix_stream(const MixParams& p, const MixRun& w, const unsigned char* incb,
+                                           uint32_t* my_first, const unsigned char* lut,
+                                           uint32_t lut_mask, const uint16_t* fbits, int lane) {
+  const uint32_t l4 = 4u * (uint32_t)lane, lane8 = 8u * (uint32_t)lane;
+  const uint32_t null_lv = kIdent ? kIdentNull + lane8 : kNullLv;
+  // kernel ends in a 32-wide register window: lane j holds off[kw + 1 + j]
+  uint32_t k = w.ks, kw = w.ks, kb = w.kb;
+  uint32_t ends = (uint32_t)(__ldg(p.off + min(kw + 1 + (uint32_t)lane, p.n_kernels)) - w.cs0);
+  uint32_t kend = __shfl_sync(0xffffffffu, ends, 0);
+
+  MixAcc a{};
+  uint32_t cs = 0, slot = 0;
+  while (true) {
+    const uint32_t ce = cs + kChunk;
+    cp_async_wait<kDepth - 1>();
+    uint32_t r[8], lv[8];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint4 v = w.my_ring[64 * slot + 32 * u];
+      r[4 * u + 0] = v.x; r[4 * u + 1] = v.y; r[4 * u + 2] = v.z; r[4 * u + 3] = v.w;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) lv[e] = kIdent ? ident_offset(r[e], lane8) : (uint32_t)lut[r[e] & lut_mask];
+    {
+      // refill this slot with chunk c + kDepth (the records are in registers)
+      const uint32_t nb = cs + kDepth * kChunk;
+      const uint4* src = w.gsrc + (size_t)(nb / 4);
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        cp_async16(w.ring_s + 16u * (64u * slot + 32u * u), src + 32 * u,
+                   nb + 128u * u + l4 < w.re ? 16u : 0u);
+      cp_async_commit();
+      slot = slot + 1 == kDepth ? 0 : slot + 1;
+    }
+    if (kb <= cs && ce < kend) {
+      // fast path: the whole chunk lies inside kernel k, which continues
+#pragma unroll
+      for (int e = 0; e < 8; ++e) a.regs += r[e] >> 17;
+      count_piece<kIdent>(a, lv, incb, my_first + 24, lane);
+    } else if (kb <= cs && ce <= w.re && kend < ce && k + 1 - kw < 32u &&
+               __shfl_sync(0xffffffffu, ends, (int)(k + 1 - kw)) > ce) {
+      // the common boundary chunk: kernel k (begun earlier) ends at sp inside
+      // it and kernel k + 1 runs past its end -- one pass sums the chunk and
+      // the piece before sp; k + 1's piece is the difference (per nibble:
+      // <= 8 records each, so no borrows)
+      const uint32_t sp = kend - cs;
+      uint32_t a0 = 0, a1 = 0, p0 = 0, p1 = 0, ra = 0, rp = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint32_t pic = 128u * (uint32_t)(e >> 2) + l4 + (uint32_t)(e & 3);
+        uint32_t dx, dy;
+        increment<kIdent>(lv[e], e, incb, dx, dy);
+        const uint32_t rg = r[e] >> 17;
+        a0 += dx;
+        a1 += dy;
+        ra += rg;
+        if (pic < sp) {
+          p0 += dx;
+          p1 += dy;
+          rp += rg;
+        }
+      }
+      add_piece(a, p0, p1, my_first + 24, lane);
+      a.regs += rp;
+      finish_kernel<kIdent>(a, my_first, p.out + k, p.instr + (w.cs0 + kb), kend - kb, lut,
+                            lut_mask, fbits, lane);
+      ++k;
+      kb = kend;
+      kend = __shfl_sync(0xffffffffu, ends, (int)(k - kw));
+      add_piece(a, a0 - p0, a1 - p1, my_first + 24, lane);
+      a.regs += ra - rp;
+    } else {
+      while (true) {
+        const uint32_t lo = cs > kb ? cs : kb, hi = ce < kend ? ce : kend;
+        if (lo < hi) {
+          const uint32_t plo = lo - cs, phi = hi - cs;
+          uint32_t mv[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const uint32_t pic = 128u * (uint32_t)(e >> 2) + l4 + (uint32_t)(e & 3);
+            const bool in = pic - plo < phi - plo;           // plo <= pic < phi
+            mv[e] = in ? lv[e] : null_lv;
+            a.regs += in ? (r[e] >> 17) : 0u;
+          }
+          count_piece<kIdent>(a, mv, incb, my_first + 24, lane);
+        }
+        if (kend > ce) break;                                // kernel continues in the next chunk
+        finish_kernel<kIdent>(a, my_first, p.out + k, p.instr + (w.cs0 + kb), kend - kb, lut,
+                              lut_mask, fbits, lane);
+        if (++k == w.ke) {
+          cp_async_wait<0>();
+          return;
+        }
+        kb = kend;
+        if (k - kw == 32) {                                  // next window of kernel ends
+          kw = k;
+          ends = (uint32_t)(__ldg(p.off + min(kw + 1 + (uint32_t)lane, p.n_kernels)) - w.cs0);
+        }
+        kend = __shfl_sync(0xffffffffu, ends, (int)(k - kw));
+      }
+    }
+    cs = ce;
+  }
+}
+
+template <int kDepth, bool kMayIdent>
 __global__ void __launch_bounds__(kMixThreads, 1) mix_reduce_kernel(const __grid_constant__ MixParams p,
                                                                      uint32_t lut_mask) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* inc = reinterpret_cast<uint64_t*>(smem);
-  uint32_t* firsts = reinterpret_cast<uint32_t*>(inc + 64 * 32);
-  uint4* ring = reinterpret_cast<uint4*>(smem + mix_ring_offset());
+  uint32_t* firsts = reinterpret_cast<uint32_t*>(smem + mix_inc_bytes(kMayIdent));
+  uint4* ring = reinterpret_cast<uint4*>(smem + mix_ring_offset(kMayIdent));
   unsigned char* lut = reinterpret_cast<unsigned char*>(ring + (size_t)kWarps * kDepth * (kChunk / 4));
   const int lane = threadIdx.x & 31;
   const uint32_t warps_total = gridDim.x * kWarps;
@@ -281,27 +442,14 @@ __global__ void __launch_bounds__(kMixThreads, 1) mix_reduce_kernel(const __grid
     ke = __shfl_sync(0xffffffffu, r, 16);
   }
 
-  // increment table indexed by class-table byte / 4 (= c + 32 * guard):
-  // entries 15..31 and 47..63 are zero (31 = the null entry).  Replicated
-  // per lane ([entry][lane], 16 KB): lane l reads banks 2l, 2l+1 only, so an
-  // LDS.64 of 32 lanes is two conflict-free wavefronts whatever the classes.
-  for (uint32_t i = threadIdx.x; i < 64 * 32; i += blockDim.x) {
-    const uint32_t e = i >> 5, c = e & 31u, g = e >> 5;
-    uint64_t v = 0;
-    if (c < 15) {
-      v = 1ull << (4 * c);
-      if (g && !(c >= 11 && c <= 13)) v += (1ull << (4 * kPred)) + (1ull << 60);  // PredIns + marker
-    }
-    inc[i] = v;
-  }
-  for (uint32_t i = threadIdx.x; i < kWarps * kFirstStride; i += blockDim.x) firsts[i] = kAbsent;
   // class table indexed by the record's low 17 bits (sig << 1 | guard) and
-  // the mask lut_mask (power of two - 1 >= 2*n_sig + 1): entry = 8 * (class
-  // | 16 when the guard adds a PredIns), i.e. the byte offset of the
-  // increment.  Signatures >= n_sig count as Unclassified (out-of-range ids
-  // are a caller error; the mask keeps them inside the table).
+  // the mask lut_mask (power of two - 1 >= 2*n_sig + 1): entry = 4 * class
+  // | 128 when the guard adds a PredIns (mix.py:258-259: not for CTRL
+  // classes 11-13).  Signatures >= n_sig count as Unclassified (out-of-range
+  // ids are a caller error; the mask keeps them inside the table).
   const uint32_t words = (lut_mask + 1) / 8;                // 4 signatures per word pair
   const bool lut_vec = (reinterpret_cast<uintptr_t>(p.sig_class) & 3u) == 0;
+  bool ident = kMayIdent;   // the table is the identity over its n_sig == 15 entries
   for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) {
     uint32_t w4 = 0;
     if (4 * i < p.n_sig) {
@@ -318,15 +466,51 @@ __global__ void __launch_bounds__(kMixThreads, 1) mix_reduce_kernel(const __grid
     for (int b = 0; b < 4; ++b) {
       const uint32_t sig = 4 * i + (uint32_t)b;
       const uint32_t c = sig < p.n_sig ? ((w4 >> (8 * b)) & 15u) : 14u;
+      if (sig < p.n_sig && ((w4 >> (8 * b)) & 0xffu) != sig) ident = false;
       const uint32_t g = (c < 11 || c == 14) ? 16u : 0u;
       const uint32_t pair = (c << 2) | (((c << 2) | (g << 3)) << 8);   // byte: 4c | guard<<7
       if (b & 1) o[b >> 1] |= pair << 16; else o[b >> 1] = pair;
     }
     *reinterpret_cast<uint2*>(lut + 8 * i) = make_uint2(o[0], o[1]);
   }
+  ident = kMayIdent && __syncthreads_and(ident) != 0;
+
+  // increment table, replicated per lane ([entry][lane]): lane l reads banks
+  // 2l, 2l+1 only, so an LDS.64 of 32 lanes is two conflict-free wavefronts
+  // whatever the classes.  Indexed by class-table byte / 4 (= c + 32 *
+  // guard; entries 15..31 and 47..63 are zero, 31 = the null entry), or for
+  // class records by the record's low byte (sig' = byte >> 1 & 31: the
+  // class-table lookup of the same record under lut_mask = 63, 256 = null).
+  const uint32_t n_inc = (ident ? kIdentEntries : 64u) * 32u;
+  for (uint32_t i = threadIdx.x; i < n_inc; i += blockDim.x) {
+    const uint32_t e = i >> 5;
+    uint32_t c, g;
+    if (ident) {
+      const uint32_t s = e >> 1 & 31u;
+      c = e >= 256u ? 15u : (s < 15u ? s : 14u);
+      g = e & 1u;
+    } else {
+      c = e & 31u;
+      g = e >> 5;
+    }
+    uint64_t v = 0;
+    if (c < 15) {
+      v = 1ull << (4 * c);
+      if (g && !(c >= 11 && c <= 13)) v += (1ull << (4 * kPred)) + (1ull << 60);  // PredIns + marker
+    }
+    inc[i] = v;
+  }
+  // class records: first_keys()' class mask per low byte (bit c, bit 15 =
+  // a counted guard), after the increments
+  uint16_t* fbits = reinterpret_cast<uint16_t*>(inc + kIdentEntries * 32u);
+  if (ident)
+    for (uint32_t i = threadIdx.x; i < 256u; i += blockDim.x) {
+      const uint32_t s = i >> 1 & 31u, c = s < 15u ? s : 14u;
+      fbits[i] = (uint16_t)((1u << c) | ((i & 1u) && !(c >= 11 && c <= 13) ? 0x8000u : 0u));
+    }
+  for (uint32_t i = threadIdx.x; i < kWarps * kFirstStride; i += blockDim.x) firsts[i] = kAbsent;
   __syncthreads();
   if (ks >= ke) return;
-  const unsigned char* incb = reinterpret_cast<const unsigned char*>(inc) + 8 * lane;
   uint32_t* my_first = firsts + (threadIdx.x >> 5) * kFirstStride;
 
   // Positions are kept relative to the warp's first chunk start cs0 (u32:
@@ -335,88 +519,33 @@ __global__ void __launch_bounds__(kMixThreads, 1) mix_reduce_kernel(const __grid
   // of chunk c, copied by the lane itself into its slots of the warp's
   // ring (cp.async, zero-fill past the end), so only the lane's own
   // wait_group orders them -- no barriers.
+  MixRun w;
   const uint64_t rs = __ldg(p.off + ks);
   const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(p.instr) >> 2) & 3u;
-  const uint64_t cs0 = ((rs + mis) & ~3ull) - mis;         // may be "-mis" (wraps; used as an offset)
-  const uint32_t re = (uint32_t)(__ldg(p.off + ke) - cs0);
-  const uint4* gsrc = reinterpret_cast<const uint4*>(p.instr + cs0) + lane;   // vector 64c + 32u
-  uint4* my_ring = ring + (size_t)(threadIdx.x >> 5) * kDepth * (kChunk / 4) + lane;
-  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(my_ring);
+  w.cs0 = ((rs + mis) & ~3ull) - mis;                      // may be "-mis" (wraps; used as an offset)
+  w.re = (uint32_t)(__ldg(p.off + ke) - w.cs0);
+  w.gsrc = reinterpret_cast<const uint4*>(p.instr + w.cs0) + lane;   // vector 64c + 32u
+  w.my_ring = ring + (size_t)(threadIdx.x >> 5) * kDepth * (kChunk / 4) + lane;
+  w.ring_s = (uint32_t)__cvta_generic_to_shared(w.my_ring);
+  w.kb = (uint32_t)(rs - w.cs0);
+  w.ks = ks;
+  w.ke = ke;
   const uint32_t l4 = 4u * (uint32_t)lane;
 #pragma unroll
   for (int d = 0; d < kDepth; ++d) {
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const uint32_t i = (uint32_t)d * kChunk + 128u * u + l4;
-      cp_async16(ring_s + 16u * (64u * d + 32u * u), gsrc + 64 * d + 32 * u, i < re ? 16u : 0u);
+      cp_async16(w.ring_s + 16u * (64u * d + 32u * u), w.gsrc + 64 * d + 32 * u, i < w.re ? 16u : 0u);
     }
     cp_async_commit();
   }
-  // kernel ends in a 32-wide register window: lane j holds off[kw + 1 + j]
-  uint32_t k = ks, kw = ks;
-  uint32_t ends = (uint32_t)(__ldg(p.off + min(kw + 1 + (uint32_t)lane, p.n_kernels)) - cs0);
-  uint32_t kb = (uint32_t)(rs - cs0), kend = __shfl_sync(0xffffffffu, ends, 0);
-
-  MixAcc a{};
-  uint32_t cs = 0, slot = 0;
-  while (true) {
-    const uint32_t ce = cs + kChunk;
-    cp_async_wait<kDepth - 1>();
-    uint32_t r[8], lv[8];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const uint4 v = my_ring[64 * slot + 32 * u];
-      r[4 * u + 0] = v.x; r[4 * u + 1] = v.y; r[4 * u + 2] = v.z; r[4 * u + 3] = v.w;
-    }
-#pragma unroll
-    for (int e = 0; e < 8; ++e) lv[e] = lut[r[e] & lut_mask];
-    {
-      // refill this slot with chunk c + kDepth (the records are in registers)
-      const uint32_t nb = cs + kDepth * kChunk;
-      const uint4* src = gsrc + (size_t)(nb / 4);
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-        cp_async16(ring_s + 16u * (64u * slot + 32u * u), src + 32 * u,
-                   nb + 128u * u + l4 < re ? 16u : 0u);
-      cp_async_commit();
-      slot = slot + 1 == kDepth ? 0 : slot + 1;
-    }
-    if (kb <= cs && ce < kend) {
-      // fast path: the whole chunk lies inside kernel k, which continues
-#pragma unroll
-      for (int e = 0; e < 8; ++e) a.regs += r[e] >> 17;
-      count_piece(a, lv, incb, my_first, cs - kb, lane);
-    } else {
-      while (true) {
-        const uint32_t lo = cs > kb ? cs : kb, hi = ce < kend ? ce : kend;
-        if (lo < hi) {
-          const uint32_t plo = lo - cs, phi = hi - cs;
-          uint32_t mv[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const uint32_t pic = 128u * (uint32_t)(e >> 2) + l4 + (uint32_t)(e & 3);
-            const bool in = pic - plo < phi - plo;           // plo <= pic < phi
-            mv[e] = in ? lv[e] : kNullLv;
-            a.regs += in ? (r[e] >> 17) : 0u;
-          }
-          count_piece(a, mv, incb, my_first, cs - kb, lane);
-        }
-        if (kend > ce) break;                                // kernel continues in the next chunk
-        finish_kernel(a, my_first, p.out + k, kend - kb, lane);
-        if (++k == ke) {
-          cp_async_wait<0>();
-          return;
-        }
-        kb = kend;
-        if (k - kw == 32) {                                  // next window of kernel ends
-          kw = k;
-          ends = (uint32_t)(__ldg(p.off + min(kw + 1 + (uint32_t)lane, p.n_kernels)) - cs0);
-        }
-        kend = __shfl_sync(0xffffffffu, ends, (int)(k - kw));
-      }
-    }
-    cs = ce;
-  }
+  if (kMayIdent && ident)
+    mix_stream<true, kDepth>(p, w, reinterpret_cast<const unsigned char*>(inc), my_first, lut,
+                             lut_mask, fbits, lane);
+  else
+    mix_stream<false, kDepth>(p, w, reinterpret_cast<const unsigned char*>(inc) + 8 * lane,
+                              my_first, lut, lut_mask, fbits, lane);
 }
 
 }  // namespace
@@ -438,18 +567,23 @@ extern "C" int occx_mix_reduce(const occx_ctx* ctx, const uint32_t* d_instr,
   uint32_t lut_bytes = 64;                                 // power of two >= 2 * (n_sig + 1)
   while (lut_bytes < 2 * (n_sig + 1)) lut_bytes <<= 1;
   const bool deep = lut_bytes <= 64 * 1024;
+  const bool may_ident = n_sig == 15;                      // a 15-entry table may be the identity
   const size_t ring = (size_t)kWarps * (deep ? 4 : 2) * kChunk * 4;
-  const size_t smem = mix_ring_offset() + ring + lut_bytes;
-  const void* fn = deep ? (const void*)mix_reduce_kernel<4> : (const void*)mix_reduce_kernel<2>;
+  const size_t smem = mix_ring_offset(may_ident) + ring + lut_bytes;
+  const void* fn = may_ident ? (const void*)mix_reduce_kernel<4, true>
+                   : deep    ? (const void*)mix_reduce_kernel<4, false>
+                             : (const void*)mix_reduce_kernel<2, false>;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return OCCX_ERR_CUDA;
   // persistent: one 32-warp CTA per SM (one copy of the class table per SM)
   const uint32_t grid = (uint32_t)ctx->sm_count;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (deep)
-    mix_reduce_kernel<4><<<grid, kMixThreads, smem, st>>>(p, lut_bytes - 1);
+  if (may_ident)
+    mix_reduce_kernel<4, true><<<grid, kMixThreads, smem, st>>>(p, lut_bytes - 1);
+  else if (deep)
+    mix_reduce_kernel<4, false><<<grid, kMixThreads, smem, st>>>(p, lut_bytes - 1);
   else
-    mix_reduce_kernel<2><<<grid, kMixThreads, smem, st>>>(p, lut_bytes - 1);
+    mix_reduce_kernel<2, false><<<grid, kMixThreads, smem, st>>>(p, lut_bytes - 1);
   OCCX_CUDA_TRY(cudaGetLastError());
   return OCCX_OK;
 }
