@@ -8,16 +8,17 @@
 //       counts[PredIns] += 1        CATEGORY_OF.get(UNCLASSIFIED) is None)
 //   reg_operands += regops         mix.py:260
 //
-// Work split (record-balanced, segmented): warp w of the persistent grid
-// owns the kernels whose first record lies in [off0 + w*N/W, off0 +
-// (w+1)*N/W) -- found by a 16-ary lower_bound per half-warp -- and streams
+// Work split (cost-balanced, segmented): warp w of the persistent grid
+// owns the kernels k whose key off[k] + kKernelWeight * k lies in the w-th
+// of W equal slices of the key range -- found by a 16-ary lower_bound per
+// half-warp -- and streams
 // that run of kernels as ONE contiguous record range in 256-record chunks,
 // two LDG.128 per lane, the next chunk in flight while the current one is
 // counted.  Chunks fully inside one kernel (the common case) are counted
 // without masks; a chunk holding kernel boundaries is counted piece by piece
-// with position masks.  Every warp gets ~N/W records (at most one kernel
-// more), so unequal kernel lengths do not leave a tail, and no kernel pads
-// its last chunk.
+// with position masks.  Every warp gets ~1/W of the records-plus-kernels
+// cost (at most one kernel more), so unequal kernel lengths do not leave a
+// tail, and no kernel pads its last chunk.
 //
 // Counting: the class table holds, per (signature, guard), one byte
 // 4c | 128g (c = class, g = the guard adds a PredIns); 0x7c is "not in this
@@ -92,8 +93,19 @@ __device__ __forceinline__ void reduce_counters_eo(const uint32_t (&w)[4], int l
   total += v;
 }
 
-// lower_bound: smallest k in [0, n] with off[k] >= bound (off[n] >= bound
-// holds).  Each half-warp searches its own bound, 16 probes per round.
+// Work split: a kernel costs about as much fixed work (boundary pieces,
+// counter reduction, first-position rescan, output) as kKernelWeight
+// records, so warps are balanced on off[k] + kKernelWeight * k (monotone in
+// k) rather than on records alone: record-balanced runs varied by 14-33
+// kernels per warp on config 3.
+#ifndef OCCX_K0_KW
+#define OCCX_K0_KW 1024
+#endif
+constexpr uint64_t kKernelWeight = OCCX_K0_KW;
+
+// lower_bound: smallest k in [0, n] with off[k] + kKernelWeight * k >=
+// bound (k = n satisfies it).  Each half-warp searches its own bound, 16
+// probes per round.
 __device__ __forceinline__ uint32_t seg_search(const uint64_t* off, uint32_t n, uint64_t bound,
                                                int lane) {
   const int half = lane >> 4, sub = lane & 15;
@@ -101,7 +113,7 @@ __device__ __forceinline__ uint32_t seg_search(const uint64_t* off, uint32_t n, 
   while (__any_sync(0xffffffffu, hi > lo)) {
     const uint32_t span = hi - lo;
     const uint32_t probe = lo + (uint32_t)(((uint64_t)span * (uint32_t)(sub + 1)) >> 4);
-    const unsigned b = __ballot_sync(0xffffffffu, __ldg(off + probe) >= bound);
+    const unsigned b = __ballot_sync(0xffffffffu, __ldg(off + probe) + kKernelWeight * probe >= bound);
     const int f = __ffs((b >> (16 * half)) & 0xffffu) - 1;   // >= 0: probe 15 is hi
     const uint32_t pf = __shfl_sync(0xffffffffu, probe, 16 * half + f);
     const uint32_t pp = __shfl_sync(0xffffffffu, probe, 16 * half + (f > 0 ? f - 1 : 0));
@@ -435,7 +447,8 @@ __global__ void __launch_bounds__(kMixThreads, 1) mix_reduce_kernel(const __grid
   uint32_t ks, ke;
   {
     const uint32_t w = gw + (uint32_t)(lane >> 4);
-    const uint64_t bound = base + (n_rec * (uint64_t)w) / warps_total;   // n_rec < 2^32
+    const uint64_t total = n_rec + kKernelWeight * p.n_kernels;          // < 2^42
+    const uint64_t bound = base + (total * (uint64_t)w) / warps_total;
     uint32_t r = seg_search(p.off, p.n_kernels, bound, lane);
     if (w >= warps_total) r = p.n_kernels;                 // trailing empty kernels: last warp
     ks = __shfl_sync(0xffffffffu, r, 0);

@@ -219,6 +219,48 @@ def test_k0_ragged_segments_vs_oracle(seed):
         _k0_check(out, rec, off, lut)
 
 
+@pytest.mark.parametrize("table", ["identity", "permuted", "random"])
+@pytest.mark.parametrize("kind", range(3))
+def test_k0_fifteen_entry_tables_vs_oracle(table, kind):
+    """15-entry class tables: the identity (class records, what the
+    tokenizer emits -- K0 indexes its increment table by the record's low
+    byte) and two 15-entry tables that are not the identity (the same
+    kernel instance, generic lookup path).  Ids 15..31 are past the table
+    (Unclassified); ragged layouts as above, misaligned buffers."""
+    from paper_1701_08547_b200 import batch
+    rng = np.random.default_rng(77 + 10 * kind + len(table))
+    lut = {"identity": np.arange(15), "permuted": rng.permutation(15),
+           "random": rng.integers(0, 15, 15)}[table].astype(np.uint8)
+    if table == "identity":
+        np.testing.assert_array_equal(lut, batch.CLASS_LUT)
+    n_k = int(rng.integers(1, 4000))
+    if kind == 0:
+        lens = rng.integers(0, 300, n_k) * (rng.random(n_k) > 0.2)
+    elif kind == 1:
+        lens = rng.integers(32, 2048, n_k)
+        lens[rng.integers(0, n_k, 2)] = rng.integers(100_000, 900_000, 2)
+    else:
+        lens = rng.integers(1, 5000, n_k)
+        lens[:3] = 0
+        lens[-4:] = 0
+    n_rec = int(lens.sum())
+    lead = int(rng.integers(0, 9))
+    # mostly common classes, a few rare ones (late first occurrences)
+    p = np.r_[np.full(15, 1.0), np.full(17, 0.02)]
+    p[rng.integers(0, 15, 4)] = 0.001
+    sig = rng.choice(32, n_rec + lead, p=p / p.sum()).astype(np.uint32)
+    regops = rng.integers(0, 256, n_rec + lead).astype(np.uint32)
+    guard = (rng.random(n_rec + lead) < 0.2).astype(np.uint32)
+    rec = guard | (sig << 1) | (regops << 17)
+    off = (lead + np.concatenate([[0], np.cumsum(lens)])).astype(np.uint64)
+    for mis in (0, 3):
+        buf = np.zeros(len(rec) + 4, np.uint32)
+        buf[mis:mis + len(rec)] = rec
+        d = batch._to_device(buf)
+        out = _k0_run(d[4 * mis:], off, lut)
+        _k0_check(out, rec, off, lut)
+
+
 def random_big_block_config(rng, n_arch=3, n_kern=2):
     """Spaces whose (REGS x SMEM) blocks span many 128-candidate slices, so
     K2i's separable-table path runs; block sizes are not multiples of 128
