@@ -528,6 +528,51 @@ def secondary_records(name: str, mode: str, hbm_peak: float, steps: int = 20):
             "cpu_baseline": cpu_reference(name, mode, 1_000_000)}
 
 
+def secondary_config5_shards(plan, records, full_ms: float, hbm_peak: float, reps: int = 10):
+    """Each rank's share of config 5 under strong scaling at G = 2 / 4 / 8,
+    timed on this GPU (one process per shard is what the N-GPU run does;
+    this box has one GPU): K2 + K3 over the shard's contiguous index range
+    of the resident records (dist.shard_range), back-to-back launches.
+    ``rate_vs_full`` = the shard's candidates/s over the full-size step's;
+    the slowest shard bounds the G-GPU step before the all-gather."""
+    import torch
+    from paper_1701_08547_b200.dist import shard_range
+    tab = torch.empty((plan.n_seg, plan.k), dtype=torch.int64, device="cuda")
+    full_rate = plan.total / full_ms
+
+    def shard_ms(b, n):
+        view = records[16 * b:]
+        for _ in range(3):
+            plan.merge(plan.score_partials(view, n, index_base=b), plan.grid_lists, out=tab)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            plan.merge(plan.score_partials(view, n, index_base=b), plan.grid_lists, out=tab)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    out = {"workload": "config5-1e9-orio-space, strong-scaling shards",
+           "full_ms": full_ms, "unit": UNIT}
+    for G in (2, 4, 8):
+        ts, ns = [], []
+        for g in range(G):
+            b, e = shard_range(plan.total, g, G)
+            ts.append(shard_ms(b, e - b))
+            ns.append(e - b)
+        slow = max(range(G), key=lambda g: ts[g])
+        out[f"G{G}"] = {
+            "shard_candidates": ns[0], "shard_ms": ts,
+            "slowest_ms": ts[slow],
+            "shard0_rate_vs_full": (ns[0] / ts[0]) / full_rate,
+            "slowest_rate_vs_full": (ns[slow] / ts[slow]) / full_rate,
+            "projected_k2k3_efficiency": full_ms / G / ts[slow],
+            "slowest_frac": 16 * ns[slow] / (ts[slow] / 1e3) / 1e9 / hbm_peak}
+    out["note"] = ("K2 + K3 per shard (no all-gather); VERDICT r01 asked for the 160,563,200-"
+                   "candidate shard (G8, begin = 0) at >= 0.95 of the full-size rate")
+    return out
+
+
 def secondary_suggest(mode: str, n_kernels: int = 100_000, steps: int = 20):
     """K4 (batched suggest()): Table VI outputs for a
     100k-kernel corpus on the five config archs (500k requests; registers
@@ -967,7 +1012,10 @@ def main():
                          ("implicit_grid_score_space", lambda: secondary_space_api(cfg, args.mode)),
                          ("config4_records", lambda: secondary_records("config4", args.mode, hbm_peak)),
                          ("suggest_100k_kernels", lambda: secondary_suggest(args.mode)),
-                         ("config2_records", lambda: secondary_records("config2", args.mode, hbm_peak))):
+                         ("config2_records", lambda: secondary_records("config2", args.mode, hbm_peak)),
+                         ("config5_shards", lambda: secondary_config5_shards(plan, records, ms_max,
+                                                                             hbm_peak)
+                          if args.workload == "config5" else {"skipped": "config 5 only"})):
             try:
                 secondary[name] = fn()
             except Exception as exc:

@@ -455,6 +455,37 @@ __global__ void __launch_bounds__(kMixThreads, 1) mix_reduce_kernel(const __grid
     ke = __shfl_sync(0xffffffffu, r, 16);
   }
 
+  // Positions are kept relative to the warp's first chunk start cs0 (u32:
+  // a call holds < 2^32 records).  The chunk grid is aligned to 16-byte
+  // addresses; lane holds records c + 128u + 4*lane + j (u = 0, 1; j = 0..3)
+  // of chunk c, copied by the lane itself into its slots of the warp's
+  // ring (cp.async, zero-fill past the end), so only the lane's own
+  // wait_group orders them -- no barriers.
+  MixRun w;
+  const uint64_t rs = __ldg(p.off + ks);
+  const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(p.instr) >> 2) & 3u;
+  w.cs0 = ((rs + mis) & ~3ull) - mis;                      // may be "-mis" (wraps; used as an offset)
+  w.re = (uint32_t)(__ldg(p.off + ke) - w.cs0);
+  w.gsrc = reinterpret_cast<const uint4*>(p.instr + w.cs0) + lane;   // vector 64c + 32u
+  w.my_ring = ring + (size_t)(threadIdx.x >> 5) * kDepth * (kChunk / 4) + lane;
+  w.ring_s = (uint32_t)__cvta_generic_to_shared(w.my_ring);
+  w.kb = (uint32_t)(rs - w.cs0);
+  w.ks = ks;
+  w.ke = ke;
+  // the ring fill goes out before the tables are built (its DRAM latency
+  // covers them)
+  const uint32_t l4 = 4u * (uint32_t)lane;
+#pragma unroll
+  for (int d = 0; d < kDepth; ++d) {
+    if (ks >= ke) break;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint32_t i = (uint32_t)d * kChunk + 128u * u + l4;
+      cp_async16(w.ring_s + 16u * (64u * d + 32u * u), w.gsrc + 64 * d + 32 * u, i < w.re ? 16u : 0u);
+    }
+    cp_async_commit();
+  }
+
   // class table indexed by the record's low 17 bits (sig << 1 | guard) and
   // the mask lut_mask (power of two - 1 >= 2*n_sig + 1): entry = 4 * class
   // | 128 when the guard adds a PredIns (mix.py:258-259: not for CTRL
@@ -526,33 +557,6 @@ __global__ void __launch_bounds__(kMixThreads, 1) mix_reduce_kernel(const __grid
   if (ks >= ke) return;
   uint32_t* my_first = firsts + (threadIdx.x >> 5) * kFirstStride;
 
-  // Positions are kept relative to the warp's first chunk start cs0 (u32:
-  // a call holds < 2^32 records).  The chunk grid is aligned to 16-byte
-  // addresses; lane holds records c + 128u + 4*lane + j (u = 0, 1; j = 0..3)
-  // of chunk c, copied by the lane itself into its slots of the warp's
-  // ring (cp.async, zero-fill past the end), so only the lane's own
-  // wait_group orders them -- no barriers.
-  MixRun w;
-  const uint64_t rs = __ldg(p.off + ks);
-  const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(p.instr) >> 2) & 3u;
-  w.cs0 = ((rs + mis) & ~3ull) - mis;                      // may be "-mis" (wraps; used as an offset)
-  w.re = (uint32_t)(__ldg(p.off + ke) - w.cs0);
-  w.gsrc = reinterpret_cast<const uint4*>(p.instr + w.cs0) + lane;   // vector 64c + 32u
-  w.my_ring = ring + (size_t)(threadIdx.x >> 5) * kDepth * (kChunk / 4) + lane;
-  w.ring_s = (uint32_t)__cvta_generic_to_shared(w.my_ring);
-  w.kb = (uint32_t)(rs - w.cs0);
-  w.ks = ks;
-  w.ke = ke;
-  const uint32_t l4 = 4u * (uint32_t)lane;
-#pragma unroll
-  for (int d = 0; d < kDepth; ++d) {
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const uint32_t i = (uint32_t)d * kChunk + 128u * u + l4;
-      cp_async16(w.ring_s + 16u * (64u * d + 32u * u), w.gsrc + 64 * d + 32 * u, i < w.re ? 16u : 0u);
-    }
-    cp_async_commit();
-  }
   if (kMayIdent && ident)
     mix_stream<true, kDepth>(p, w, reinterpret_cast<const unsigned char*>(inc), my_first, lut,
                              lut_mask, fbits, lane);
