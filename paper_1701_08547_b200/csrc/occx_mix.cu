@@ -107,21 +107,26 @@ constexpr uint64_t kKernelWeight = OCCX_K0_KW;
 // bound (k = n satisfies it).  Each half-warp searches its own bound, 16
 // probes per round.
 __device__ __forceinline__ uint32_t seg_search(const uint64_t* off, uint32_t n, uint64_t bound,
-                                               int lane) {
+                                               uint64_t off_n, uint64_t& off_lo, int lane) {
   const int half = lane >> 4, sub = lane & 15;
   uint32_t lo = 0, hi = n;
+  uint64_t hv = off_n;                                     // off[hi]
   while (__any_sync(0xffffffffu, hi > lo)) {
     const uint32_t span = hi - lo;
     const uint32_t probe = lo + (uint32_t)(((uint64_t)span * (uint32_t)(sub + 1)) >> 4);
-    const unsigned b = __ballot_sync(0xffffffffu, __ldg(off + probe) + kKernelWeight * probe >= bound);
+    const uint64_t v = __ldg(off + probe);
+    const unsigned b = __ballot_sync(0xffffffffu, v + kKernelWeight * probe >= bound);
     const int f = __ffs((b >> (16 * half)) & 0xffffu) - 1;   // >= 0: probe 15 is hi
     const uint32_t pf = __shfl_sync(0xffffffffu, probe, 16 * half + f);
+    const uint64_t vf = __shfl_sync(0xffffffffu, v, 16 * half + f);
     const uint32_t pp = __shfl_sync(0xffffffffu, probe, 16 * half + (f > 0 ? f - 1 : 0));
     if (hi > lo) {
       lo = f > 0 ? pp + 1 : lo;
       hi = pf;
+      hv = vf;
     }
   }
+  off_lo = hv;                                             // lo == hi: off[lo], no extra load
   return lo;
 }
 
@@ -445,14 +450,21 @@ __global__ void __launch_bounds__(kMixThreads, 1) mix_reduce_kernel(const __grid
     return;
   }
   uint32_t ks, ke;
+  uint64_t rs, rend;
   {
     const uint32_t w = gw + (uint32_t)(lane >> 4);
     const uint64_t total = n_rec + kKernelWeight * p.n_kernels;          // < 2^42
     const uint64_t bound = base + (total * (uint64_t)w) / warps_total;
-    uint32_t r = seg_search(p.off, p.n_kernels, bound, lane);
-    if (w >= warps_total) r = p.n_kernels;                 // trailing empty kernels: last warp
+    uint64_t ov;
+    uint32_t r = seg_search(p.off, p.n_kernels, bound, base + n_rec, ov, lane);
+    if (w >= warps_total) {                                // trailing empty kernels: last warp
+      r = p.n_kernels;
+      ov = base + n_rec;
+    }
     ks = __shfl_sync(0xffffffffu, r, 0);
     ke = __shfl_sync(0xffffffffu, r, 16);
+    rs = __shfl_sync(0xffffffffu, ov, 0);                  // off[ks]
+    rend = __shfl_sync(0xffffffffu, ov, 16);               // off[ke]
   }
 
   // Positions are kept relative to the warp's first chunk start cs0 (u32:
@@ -462,10 +474,9 @@ __global__ void __launch_bounds__(kMixThreads, 1) mix_reduce_kernel(const __grid
   // ring (cp.async, zero-fill past the end), so only the lane's own
   // wait_group orders them -- no barriers.
   MixRun w;
-  const uint64_t rs = __ldg(p.off + ks);
   const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(p.instr) >> 2) & 3u;
   w.cs0 = ((rs + mis) & ~3ull) - mis;                      // may be "-mis" (wraps; used as an offset)
-  w.re = (uint32_t)(__ldg(p.off + ke) - w.cs0);
+  w.re = (uint32_t)(rend - w.cs0);
   w.gsrc = reinterpret_cast<const uint4*>(p.instr + w.cs0) + lane;   // vector 64c + 32u
   w.my_ring = ring + (size_t)(threadIdx.x >> 5) * kDepth * (kChunk / 4) + lane;
   w.ring_s = (uint32_t)__cvta_generic_to_shared(w.my_ring);
