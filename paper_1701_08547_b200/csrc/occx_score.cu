@@ -1327,6 +1327,9 @@ __global__ void __launch_bounds__(kMergeThreads)
 topk_merge_kernel(const uint64_t* __restrict__ lists, uint32_t n_lists, uint32_t n_seg, uint32_t k,
                   uint64_t* __restrict__ out) {
   __shared__ uint64_t s_w[kMergeThreads / 32][OCCX_MAX_K];
+  // launched as a programmatic dependent of the scorer: the CTAs are
+  // scheduled while the scorer's last CTAs drain; wait for its writes here
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t seg = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int kWarps = kMergeThreads / 32;
@@ -1666,9 +1669,20 @@ extern "C" int occx_topk_merge(const occx_ctx* ctx, const uint64_t* d_lists, uin
                                uint32_t n_seg, uint32_t k, uint64_t* d_out, void* stream) {
   if (!ctx || k == 0 || k > OCCX_MAX_K || n_lists == 0) return OCCX_ERR_VALUE;
   if (n_seg == 0) return OCCX_OK;
-  topk_merge_kernel<<<n_seg, kMergeThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      d_lists, n_lists, n_seg, k, d_out);
-  OCCX_CUDA_TRY(cudaGetLastError());
+  // programmatic dependent launch: K3's launch overlaps the tail of the
+  // kernel before it on the stream (K2); griddepcontrol.wait in K3 orders
+  // the reads (a no-op when the previous work is not a kernel)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(n_seg);
+  cfg.blockDim = dim3(kMergeThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = reinterpret_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  OCCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, topk_merge_kernel, d_lists, n_lists, n_seg, k, d_out));
   return OCCX_OK;
 }
 

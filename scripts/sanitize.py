@@ -67,6 +67,15 @@ def main():
     counts, _, regs = oracle.aggregate_records(rec, c.offsets, lut)
     assert np.array_equal(got["counts"][:, :15].astype(np.int64), counts), "K0 counts"
     assert np.array_equal(got["reg_operands"].astype(np.int64), regs), "K0 reg_operands"
+    # class records (identity table: the byte-indexed increment path) and a
+    # permuted 15-entry table (same kernel instance, generic lookups)
+    crec = batch.classify_records(rec, lut)
+    for tab in (batch.CLASS_LUT, np.random.default_rng(5).permutation(15).astype(np.uint8)):
+        batch.mix_reduce(batch._to_device(crec), d_off, c.n_kernels, batch._to_device(tab),
+                         len(tab), d_out=out)
+        got = batch._to_host(out, _lib.MIX, c.n_kernels)
+        counts, _, regs = oracle.aggregate_records(crec, c.offsets, tab)
+        assert np.array_equal(got["counts"][:, :15].astype(np.int64), counts), "K0 class counts"
     print("K0 ok", flush=True)
 
     # Kd + K4
