@@ -219,7 +219,10 @@ int occx_suggest_batch(const occx_ctx* ctx, const occx_arch_t* h_archs,
 
 /* ---- K0: instruction-mix reducer --------------------------------------
  * Replaces aggregate() mix.py:245-261 (classify :176-187 is the d_sig_class
- * LUT lookup).  d_kernel_off has n_kernels+1 entries (CSR).            */
+ * LUT lookup).  d_kernel_off has n_kernels+1 entries (CSR).  With the
+ * 15-entry identity table (class records, occx_sass_classify) the kernel
+ * indexes its increment table by the record's low byte; any other table,
+ * 15 entries included, takes the generic lookup -- same results.      */
 int occx_mix_reduce(const occx_ctx* ctx, const uint32_t* d_instr,
                     const uint64_t* d_kernel_off, uint32_t n_kernels,
                     const uint8_t* d_sig_class, uint32_t n_sig,
@@ -276,7 +279,9 @@ int occx_score_topk(const occx_ctx* ctx, const occx_arch_t* h_archs, int n_arch,
                     uint64_t* d_topk, void* stream);
 
 /* K3 alone: merge n_lists top-k tables [n_lists][n_seg][k] into one
- * (multi-GPU: after the all-gather of per-rank tables).                */
+ * (multi-GPU: after the all-gather of per-rank tables).  Launched as a
+ * programmatic dependent of the kernel before it on the stream (it waits
+ * for that kernel's writes before reading d_lists).                    */
 int occx_topk_merge(const occx_ctx* ctx, const uint64_t* d_lists,
                     uint32_t n_lists, uint32_t n_seg, uint32_t k,
                     uint64_t* d_out, void* stream);
