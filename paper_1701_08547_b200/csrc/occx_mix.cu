@@ -44,7 +44,13 @@ using namespace occx;
 
 namespace {
 
-constexpr int kMixThreads = 1024;
+#ifndef OCCX_K0_THREADS
+#define OCCX_K0_THREADS 1024   // one CTA per SM; 64 registers per thread
+#define OCCX_K0_DEEP 4         // ring chunks per warp (class tables <= 64 KB)
+#define OCCX_K0_SHALLOW 2      // ring chunks per warp (larger class tables)
+#endif
+constexpr int kMixThreads = OCCX_K0_THREADS;
+constexpr int kDeep = OCCX_K0_DEEP, kShallow = OCCX_K0_SHALLOW;
 constexpr int kWarps = kMixThreads / 32;
 constexpr uint32_t kChunk = 256;                      // records per warp-chunk (8 per lane)
 constexpr int kFlushPieces = 255 / 8;                 // byte counters cannot overflow
@@ -596,22 +602,22 @@ extern "C" int occx_mix_reduce(const occx_ctx* ctx, const uint32_t* d_instr,
   while (lut_bytes < 2 * (n_sig + 1)) lut_bytes <<= 1;
   const bool deep = lut_bytes <= 64 * 1024;
   const bool may_ident = n_sig == 15;                      // a 15-entry table may be the identity
-  const size_t ring = (size_t)kWarps * (deep ? 4 : 2) * kChunk * 4;
+  const size_t ring = (size_t)kWarps * (deep ? kDeep : kShallow) * kChunk * 4;
   const size_t smem = mix_ring_offset(may_ident) + ring + lut_bytes;
-  const void* fn = may_ident ? (const void*)mix_reduce_kernel<4, true>
-                   : deep    ? (const void*)mix_reduce_kernel<4, false>
-                             : (const void*)mix_reduce_kernel<2, false>;
+  const void* fn = may_ident ? (const void*)mix_reduce_kernel<kDeep, true>
+                   : deep    ? (const void*)mix_reduce_kernel<kDeep, false>
+                             : (const void*)mix_reduce_kernel<kShallow, false>;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return OCCX_ERR_CUDA;
   // persistent: one 32-warp CTA per SM (one copy of the class table per SM)
   const uint32_t grid = (uint32_t)ctx->sm_count;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (may_ident)
-    mix_reduce_kernel<4, true><<<grid, kMixThreads, smem, st>>>(p, lut_bytes - 1);
+    mix_reduce_kernel<kDeep, true><<<grid, kMixThreads, smem, st>>>(p, lut_bytes - 1);
   else if (deep)
-    mix_reduce_kernel<4, false><<<grid, kMixThreads, smem, st>>>(p, lut_bytes - 1);
+    mix_reduce_kernel<kDeep, false><<<grid, kMixThreads, smem, st>>>(p, lut_bytes - 1);
   else
-    mix_reduce_kernel<2, false><<<grid, kMixThreads, smem, st>>>(p, lut_bytes - 1);
+    mix_reduce_kernel<kShallow, false><<<grid, kMixThreads, smem, st>>>(p, lut_bytes - 1);
   OCCX_CUDA_TRY(cudaGetLastError());
   return OCCX_OK;
 }
