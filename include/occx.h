@@ -347,7 +347,7 @@ int occx_gen_space(const occx_ctx* ctx, const occx_segdesc_t* d_desc,
  * occx_sass_free (also call it after errors).                           */
 typedef struct occx_sass occx_sass;
 int occx_sass_parse(const char* utf8, uint64_t n_bytes, occx_sass** out, int64_t* err_line);
-/* Same, with the minimum bytes per worker-thread chunk (0 = 4 MB default);
+/* Same, with the minimum bytes per worker-thread chunk (0 = 1 MB default);
  * small values split the text at many line boundaries (results identical). */
 int occx_sass_parse_ex(const char* utf8, uint64_t n_bytes, uint64_t chunk_bytes_min,
                        occx_sass** out, int64_t* err_line);
@@ -359,6 +359,11 @@ const char* occx_sass_kernel_name(const occx_sass* r, uint32_t k);
 uint32_t occx_sass_n_sigs(const occx_sass* r);
 const char* occx_sass_signature(const occx_sass* r, uint32_t i);
 const char* occx_sass_error_text(const occx_sass* r);
+/* All kernel names / all signatures in one buffer, joined by 0x1E (a line
+ * break, so neither contains it); *n_bytes = its length.  One call instead
+ * of one per name / signature.                                           */
+const char* occx_sass_names_blob(const occx_sass* r, uint64_t* n_bytes);
+const char* occx_sass_signatures_blob(const occx_sass* r, uint64_t* n_bytes);
 /* Rewrite the records in place with class ids instead of signature ids
  * (sig_class[n_sig]: classify() per interned signature, mix.py:176-187;
  * values <= 14): "class records" for occx_mix_reduce with the identity

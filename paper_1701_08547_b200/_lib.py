@@ -86,6 +86,8 @@ SIGNATURES = {
     "occx_sass_n_sigs": ([_P], _U32),
     "occx_sass_signature": ([_P, _U32], ctypes.c_char_p),
     "occx_sass_error_text": ([_P], ctypes.c_char_p),
+    "occx_sass_names_blob": ([_P, _P], _P),
+    "occx_sass_signatures_blob": ([_P, _P], _P),
     "occx_sass_free": ([_P], None),
     "occx_sass_classify": ([_P, _P, _U32], _I),
     "occx_score_space": ([_P, _P, _I, _P, _U32, _P, _U32, _U64, _U64, _U64, _I, _U32, _P, _U32,

@@ -490,6 +490,7 @@ struct occx_sass {
   std::vector<std::string> sigs;
   std::string error;               // message (';' error: 0x01 + offending token)
   int64_t error_line = 0;
+  std::string names_blob, sigs_blob;   // all names / signatures joined by 0x1E
 };
 
 extern "C" int occx_sass_parse(const char* text, uint64_t n_bytes, occx_sass** out,
@@ -507,8 +508,9 @@ extern "C" int occx_sass_parse_ex(const char* text, uint64_t n_bytes, uint64_t c
   // line-aligned chunks (cut after '\n'; a "\r\n" pair never straddles a cut)
   unsigned hw = std::thread::hardware_concurrency();
   const unsigned max_t = hw ? (hw < 32 ? hw : 32) : 1;
-  // >= 4 MB per chunk by default; callers (tests) may force small chunks
-  const uint64_t chunk_bytes = chunk_bytes_min ? chunk_bytes_min : (uint64_t)(4u << 20);
+  // >= 1 MB per chunk by default (every core on mid-size listings); callers
+  // (tests) may force small chunks
+  const uint64_t chunk_bytes = chunk_bytes_min ? chunk_bytes_min : (uint64_t)(1u << 20);
   unsigned n_chunks = (unsigned)(n_bytes / chunk_bytes) + 1;
   if (n_chunks > max_t) n_chunks = max_t;
   std::vector<size_t> cut{0};
@@ -536,6 +538,11 @@ extern "C" int occx_sass_parse_ex(const char* text, uint64_t n_bytes, uint64_t c
     return OCCX_ERR_EMPTY;
   }
   std::unordered_map<std::string, uint32_t> gid;
+  {
+    size_t total = 0;
+    for (auto& c : ck) total += c.recs.size();
+    r->records.reserve(total);
+  }
   bool have_fn = false;
   std::string cur;
   uint64_t line_base = 0;
@@ -592,6 +599,16 @@ extern "C" int occx_sass_parse_ex(const char* text, uint64_t n_bytes, uint64_t c
   }
   if (have_fn) r->offsets.push_back(r->records.size());
   r->offsets.insert(r->offsets.begin(), 0);
+  // one-call views of the names and signatures (0x1E is a line break, so it
+  // occurs in neither)
+  for (size_t i = 0; i < r->names.size(); ++i) {
+    if (i) r->names_blob.push_back('\x1e');
+    r->names_blob += r->names[i];
+  }
+  for (size_t i = 0; i < r->sigs.size(); ++i) {
+    if (i) r->sigs_blob.push_back('\x1e');
+    r->sigs_blob += r->sigs[i];
+  }
   return OCCX_OK;
 }
 
@@ -611,6 +628,14 @@ extern "C" const char* occx_sass_signature(const occx_sass* r, uint32_t i) {
   return r && i < r->sigs.size() ? r->sigs[i].c_str() : nullptr;
 }
 extern "C" const char* occx_sass_error_text(const occx_sass* r) { return r ? r->error.c_str() : ""; }
+extern "C" const char* occx_sass_names_blob(const occx_sass* r, uint64_t* n_bytes) {
+  if (n_bytes) *n_bytes = r ? r->names_blob.size() : 0;
+  return r ? r->names_blob.c_str() : "";
+}
+extern "C" const char* occx_sass_signatures_blob(const occx_sass* r, uint64_t* n_bytes) {
+  if (n_bytes) *n_bytes = r ? r->sigs_blob.size() : 0;
+  return r ? r->sigs_blob.c_str() : "";
+}
 
 // Replace every record's signature id by its class id (sig_class[sig],
 // classify() of the interned signature, mix.py:176-187): "class records",

@@ -35,6 +35,13 @@ class SassRecords:
         return np.asarray(lut or [DEVICE_ID[OpClass.UNCLASSIFIED]], np.uint8)
 
 
+def _blob(fn, h) -> list:
+    """One call for all names / signatures: the library joins them by 0x1E."""
+    n = ctypes.c_uint64(0)
+    ptr = fn(h, ctypes.byref(n))
+    return ctypes.string_at(ptr, n.value).decode("utf-8", "surrogatepass").split("\x1e")
+
+
 def tokenize(text: str, chunk_bytes: int = 0, table=None) -> SassRecords:
     """``chunk_bytes``: minimum bytes per worker-thread chunk (0 = library
     default); only the split changes, never the result.  ``table`` (an
@@ -62,15 +69,15 @@ def tokenize(text: str, chunk_bytes: int = 0, table=None) -> SassRecords:
             _lib.check(st, f"occx_sass_parse (line {line.value}): {err}")
         n_k = lib.occx_sass_n_kernels(h)
         n_i = lib.occx_sass_n_instr(h)
-        names = [lib.occx_sass_kernel_name(h, k).decode("utf-8", "surrogatepass")
-                 for k in range(n_k)]
+        names = _blob(lib.occx_sass_names_blob, h) if n_k else []
         off = np.ctypeslib.as_array(ctypes.cast(lib.occx_sass_offsets(h),
                                                 ctypes.POINTER(ctypes.c_uint64)),
                                     shape=(n_k + 1,)).copy() if n_k else np.zeros(1, np.uint64)
         sigs = []
-        for i in range(lib.occx_sass_n_sigs(h)):
-            parts = lib.occx_sass_signature(h, i).decode("utf-8", "surrogatepass").split("\x1f")
-            sigs.append((parts[0], tuple("." + m for m in parts[1:])))
+        if lib.occx_sass_n_sigs(h):
+            for s in _blob(lib.occx_sass_signatures_blob, h):
+                parts = s.split("\x1f")
+                sigs.append((parts[0], tuple("." + m for m in parts[1:])))
         out = SassRecords(names, off, None, sigs)
         if table is not None and n_i:
             lut = out.class_lut(table)
