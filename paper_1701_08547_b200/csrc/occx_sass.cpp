@@ -538,11 +538,11 @@ extern "C" int occx_sass_parse_ex(const char* text, uint64_t n_bytes, uint64_t c
     return OCCX_ERR_EMPTY;
   }
   std::unordered_map<std::string, uint32_t> gid;
-  {
-    size_t total = 0;
-    for (auto& c : ck) total += c.recs.size();
-    r->records.reserve(total);
-  }
+  // serial pass: global signature ids, function starts (as output positions)
+  // and errors in chunk order; the records are copied afterwards, one thread
+  // per chunk
+  std::vector<std::vector<uint32_t>> remaps(ck.size());
+  std::vector<uint64_t> rec_base(ck.size() + 1, 0);
   bool have_fn = false;
   std::string cur;
   uint64_t line_base = 0;
@@ -552,13 +552,15 @@ extern "C" int occx_sass_parse_ex(const char* text, uint64_t n_bytes, uint64_t c
     if (err_line) *err_line = (int64_t)line;
     return status;
   };
-  for (auto& c : ck) {
+  for (size_t ci = 0; ci < ck.size(); ++ci) {
+    Chunk& c = ck[ci];
     // instructions before this chunk's first header continue the open function
     const uint64_t lead = c.fns.empty() ? c.recs.size() : c.fns[0].at;
     if (lead > 0 && !have_fn)
       return fail(OCCX_ERR_PARSE, line_base + c.first_instr_line,
                   "instruction before any function header");
-    std::vector<uint32_t> remap(c.sigs.size());
+    std::vector<uint32_t>& remap = remaps[ci];
+    remap.resize(c.sigs.size());
     for (size_t i = 0; i < c.sigs.size(); ++i) {
       auto it = gid.find(c.sigs[i]);
       if (it == gid.end()) {
@@ -571,20 +573,12 @@ extern "C" int occx_sass_parse_ex(const char* text, uint64_t n_bytes, uint64_t c
       }
       remap[i] = it->second;
     }
-    size_t f = 0;
-    for (uint64_t j = 0; j <= c.recs.size(); ++j) {
-      while (f < c.fns.size() && c.fns[f].at == j) {
-        if (!have_fn || c.fns[f].name != cur) {
-          if (have_fn) r->offsets.push_back(r->records.size());
-          r->names.push_back(c.fns[f].name);
-          cur = c.fns[f].name;
-          have_fn = true;
-        }
-        ++f;
-      }
-      if (j < c.recs.size()) {
-        const uint32_t x = c.recs[j];
-        r->records.push_back((remap[(x >> 1) & 0xffffu] << 1) | (x & 0xfffe0001u));
+    for (const FnStart& fs : c.fns) {
+      if (!have_fn || fs.name != cur) {
+        if (have_fn) r->offsets.push_back(rec_base[ci] + fs.at);
+        r->names.push_back(fs.name);
+        cur = fs.name;
+        have_fn = true;
       }
     }
     if (c.err) {
@@ -595,7 +589,21 @@ extern "C" int occx_sass_parse_ex(const char* text, uint64_t n_bytes, uint64_t c
         return fail(OCCX_ERR_ATTRIBUTE, line, "'NoneType' object has no attribute 'group'");
       return fail(OCCX_ERR_CAPACITY, line, "instruction with more than 255 register operands");
     }
+    rec_base[ci + 1] = rec_base[ci] + c.recs.size();
     line_base += c.lines;
+  }
+  r->records.resize(rec_base.back());
+  auto fill = [&](size_t ci) {
+    const std::vector<uint32_t>& remap = remaps[ci];
+    uint32_t* dst = r->records.data() + rec_base[ci];
+    for (const uint32_t x : ck[ci].recs) *dst++ = (remap[(x >> 1) & 0xffffu] << 1) | (x & 0xfffe0001u);
+  };
+  if (ck.size() == 1) {
+    fill(0);
+  } else {
+    std::vector<std::thread> th;
+    for (size_t ci = 0; ci < ck.size(); ++ci) th.emplace_back(fill, ci);
+    for (auto& t : th) t.join();
   }
   if (have_fn) r->offsets.push_back(r->records.size());
   r->offsets.insert(r->offsets.begin(), 0);

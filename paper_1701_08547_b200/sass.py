@@ -35,6 +35,26 @@ class SassRecords:
         return np.asarray(lut or [DEVICE_ID[OpClass.UNCLASSIFIED]], np.uint8)
 
 
+_AS_UTF8 = ctypes.pythonapi.PyUnicode_AsUTF8AndSize
+_AS_UTF8.restype = ctypes.c_void_p
+_AS_UTF8.argtypes = [ctypes.py_object, ctypes.POINTER(ctypes.c_ssize_t)]
+
+
+def _utf8(text: str):
+    """The listing's UTF-8 bytes without a copy where CPython has them: an
+    ASCII str stores exactly those bytes, and PyUnicode_AsUTF8AndSize hands
+    out that buffer (kept alive by ``text``).  A str with lone surrogates is
+    encoded with 'surrogatepass' (the bytes the tokenizer expects).
+    Returns (char pointer or bytes, length)."""
+    n = ctypes.c_ssize_t(0)
+    try:
+        p = _AS_UTF8(text, ctypes.byref(n))
+        return ctypes.cast(p, ctypes.c_char_p), n.value
+    except UnicodeEncodeError:
+        data = text.encode("utf-8", "surrogatepass")
+        return data, len(data)
+
+
 def _blob(fn, h) -> list:
     """One call for all names / signatures: the library joins them by 0x1E."""
     n = ctypes.c_uint64(0)
@@ -50,10 +70,10 @@ def tokenize(text: str, chunk_bytes: int = 0, table=None) -> SassRecords:
     the identity class table ``CLASS_LUT``; ``signatures`` still lists the
     interned signatures."""
     lib = _lib.load()
-    data = text.encode("utf-8", "surrogatepass")
+    data, n_bytes = _utf8(text)
     h = ctypes.c_void_p()
     line = ctypes.c_int64(0)
-    st = lib.occx_sass_parse_ex(data, len(data), int(chunk_bytes), ctypes.byref(h),
+    st = lib.occx_sass_parse_ex(data, n_bytes, int(chunk_bytes), ctypes.byref(h),
                                 ctypes.byref(line))
     try:
         if st:

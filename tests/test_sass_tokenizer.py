@@ -79,3 +79,23 @@ def test_chunked_parse_equals_single_chunk():
     single = [_summary(t) for t in texts]
     multi = [_summary(t, 97) for t in texts]
     assert multi == single
+
+
+def test_utf8_views_of_the_listing():
+    """tokenize() reads an ASCII str's own buffer, encodes other text as
+    UTF-8 and text with lone surrogates with 'surrogatepass': the three give
+    the same functions and records as the plain listing."""
+    base = ("\tFunction : kern_a\n"
+            "        /*0000*/                   MOV R1, c[0x0][0x28] ;   /* 0x1 */\n"
+            "        /*0010*/              @P0  IADD3 R2, R3, R4, RZ ;   /* 0x2 */\n"
+            "\tFunction : kern_b\n"
+            "        /*0000*/                   EXIT ;   /* 0x3 */\n")
+    want = _summary(base)
+    assert want[0] == "ok" and [n for n, _ in want[1]] == ["kern_a", "kern_b"]
+    uni = base.replace("/* 0x2 */", "/* 0x2 é☃ */")
+    sur = base.replace("/* 0x2 */", "/* 0x2 \ud800 */")
+    assert _summary(uni) == want
+    assert _summary(sur) == want
+    named = base.replace("kern_b", "kern_é")
+    got = _summary(named)
+    assert [n for n, _ in got[1]] == ["kern_a", "kern_é"] and got[1][0] == want[1][0]
