@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <string_view>
 #include <unordered_map>
 #include <functional>
 #include <algorithm>
@@ -537,7 +538,43 @@ extern "C" int occx_sass_parse_ex(const char* text, uint64_t n_bytes, uint64_t c
     r->error = "no functions found";
     return OCCX_ERR_EMPTY;
   }
-  std::unordered_map<std::string, uint32_t> gid;
+  // Global signature ids in first-occurrence order, without a serial pass
+  // over every chunk's table: partition p of P (by hash) walks the chunks in
+  // order and records, for each local signature of its partition, the
+  // (chunk, local index) of the signature's first occurrence -- its "owner".
+  // The serial pass below then numbers the owners in chunk order.
+  const size_t C = ck.size();
+  std::vector<std::vector<uint64_t>> owner(C);
+  std::vector<std::vector<size_t>> hashes(C);
+  {
+    auto hash_chunk = [&](size_t ci) {
+      hashes[ci].resize(ck[ci].sigs.size());
+      owner[ci].resize(ck[ci].sigs.size());
+      for (size_t i = 0; i < ck[ci].sigs.size(); ++i)
+        hashes[ci][i] = std::hash<std::string>{}(ck[ci].sigs[i]);
+    };
+    const unsigned P = C > 1 ? (unsigned)C : 1u;
+    auto partition = [&](unsigned part) {
+      std::unordered_map<std::string_view, uint64_t> first;
+      for (size_t ci = 0; ci < C; ++ci)
+        for (size_t i = 0; i < ck[ci].sigs.size(); ++i) {
+          if (hashes[ci][i] % P != part) continue;
+          const uint64_t key = ((uint64_t)ci << 32) | i;
+          owner[ci][i] = first.emplace(std::string_view(ck[ci].sigs[i]), key).first->second;
+        }
+    };
+    if (C == 1) {
+      hash_chunk(0);
+      partition(0);
+    } else {
+      std::vector<std::thread> th;
+      for (size_t ci = 0; ci < C; ++ci) th.emplace_back(hash_chunk, ci);
+      for (auto& t : th) t.join();
+      th.clear();
+      for (unsigned part = 0; part < P; ++part) th.emplace_back(partition, part);
+      for (auto& t : th) t.join();
+    }
+  }
   // serial pass: global signature ids, function starts (as output positions)
   // and errors in chunk order; the records are copied afterwards, one thread
   // per chunk
@@ -562,16 +599,18 @@ extern "C" int occx_sass_parse_ex(const char* text, uint64_t n_bytes, uint64_t c
     std::vector<uint32_t>& remap = remaps[ci];
     remap.resize(c.sigs.size());
     for (size_t i = 0; i < c.sigs.size(); ++i) {
-      auto it = gid.find(c.sigs[i]);
-      if (it == gid.end()) {
+      const uint64_t o = owner[ci][i];
+      const size_t oc = (size_t)(o >> 32), oi = (size_t)(o & 0xffffffffu);
+      if (oc == ci && oi == i) {                            // first occurrence: a new id
         const uint32_t id = (uint32_t)r->sigs.size();
         if (id >= 65535)
           return fail(OCCX_ERR_CAPACITY, line_base + 1,
                       "more than 65535 distinct instruction signatures");
-        it = gid.emplace(c.sigs[i], id).first;
         r->sigs.push_back(c.sigs[i]);
+        remap[i] = id;
+      } else {
+        remap[i] = remaps[oc][oi];                          // an earlier chunk (or index)
       }
-      remap[i] = it->second;
     }
     for (const FnStart& fs : c.fns) {
       if (!have_fn || fs.name != cur) {

@@ -79,6 +79,11 @@ def test_chunked_parse_equals_single_chunk():
     single = [_summary(t) for t in texts]
     multi = [_summary(t, 97) for t in texts]
     assert multi == single
+    # signature ids too: first-occurrence order whatever the chunking
+    for t in texts[-2:]:
+        a, b = sass.tokenize(t), sass.tokenize(t, 97)
+        assert a.signatures == b.signatures
+        assert np.array_equal(a.records, b.records) and np.array_equal(a.offsets, b.offsets)
 
 
 def test_utf8_views_of_the_listing():
