@@ -80,7 +80,9 @@ def test_chunked_parse_equals_single_chunk():
     multi = [_summary(t, 97) for t in texts]
     assert multi == single
     # signature ids too: first-occurrence order whatever the chunking
-    for t in texts[-2:]:
+    ok = [t for t, r in zip(texts, single) if r[0] == "ok" and len(t) > 2000]
+    assert len(ok) >= 2
+    for t in ok:
         a, b = sass.tokenize(t), sass.tokenize(t, 97)
         assert a.signatures == b.signatures
         assert np.array_equal(a.records, b.records) and np.array_equal(a.offsets, b.offsets)
