@@ -658,6 +658,7 @@ struct SepBlock {            // warp-uniform description of the tabled block
   uint32_t hi;               // the block's key bits (high word) outside the warps field
   // what the tables were built for: (T, arch, REGS pool, SMEM pool, ok)
   uint32_t kt, ka, kr, ks;
+  uint32_t rmq;              // bytes between the TS range-max levels (0: not built)
 };
 
 __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
@@ -748,6 +749,21 @@ __device__ __forceinline__ bool sep_build(const SpaceParams& q, const K2Shared& 
       sts_u32(tr + 4u * (nr + 1 + i), ok ? (aw << 22) : 0u);
     }
     __syncwarp();
+    // Range maxima over the padded TS for the quad filter: level k (k = 1..4)
+    // holds max(TS[i .. i + 2^k)), levels ns + 16 words apart.
+    const uint32_t stride = 4u * (ns + 16);
+    sb.rmq = 0;
+    if (ns >= 16 && nr + 1 + 5 * (ns + 16) <= q.sep_words) {
+      const uint32_t ts = tr + 4u * (nr + 1);
+#pragma unroll 1
+      for (uint32_t k = 1; k <= 4; ++k) {
+        const uint32_t src = ts + (k - 1) * stride, dst = ts + k * stride, half = 1u << (k - 1);
+        for (uint32_t i = (uint32_t)lane; i + 2 * half <= ns + 15; i += 32)
+          sts_u32(dst + 4u * i, max(lds_u32(src + 4u * i), lds_u32(src + 4u * (i + half))));
+        __syncwarp();
+      }
+      sb.rmq = stride;
+    }
     sb.kt = kt;
     sb.ka = a;
     sb.kr = ic.r_off | (nr << 20);
@@ -796,6 +812,7 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
   sb.n = 0;
   sb.ns = 0;
   sb.kt = sb.ka = sb.kr = sb.ks = 0xffffffffu;          // no tables yet
+  sb.rmq = 0;
   BlockBound bbnd;
   bbnd.z = 0xffffffffu;
   bbnd.w = bbnd.r_off = bbnd.s_off = bbnd.aw = 0;
@@ -888,6 +905,38 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
   };
   auto fast_quad = [&](uint64_t pb) {
     const uint32_t o8 = (uint32_t)(pb - sb.lo) + 16u * (uint32_t)lane;
+    if (sb.rmq) {
+      // Filter first from range maxima: the lane's best warps field is
+      // max(min(t0, max TS[s0, s0 + len1)), min(t1, max TS[s0 + len1, s0 + 16)))
+      // (min distributes over max) -- four LDS instead of sixteen; the
+      // per-candidate fields are only formed when some lane may offer.
+      const uint32_t r0 = fastdiv(o8, sb.ds), s0 = o8 - r0 * sb.ns;
+      const uint32_t t0 = lds_u32(tr + 4u * r0), t1 = lds_u32(tr + 4u * r0 + 4u);
+      const uint32_t len1 = min(sb.ns - s0, 16u);          // >= 1
+      const uint32_t len2 = max(16u - len1, 1u);           // (1 when unused)
+      const uint32_t k1 = 31u - __clz(len1), k2 = 31u - __clz(len2);
+      const uint32_t l1 = sb.ts + k1 * sb.rmq, l2 = sb.ts + k2 * sb.rmq;
+      const uint32_t a2 = s0 + len1;
+      const uint32_t m1 = max(lds_u32(l1 + 4u * s0), lds_u32(l1 + 4u * (a2 - (1u << k1))));
+      const uint32_t m2 = max(lds_u32(l2 + 4u * a2), lds_u32(l2 + 4u * (a2 + len2 - (1u << k2))));
+      const uint32_t m = max(min(t0, m1), len1 < 16u ? min(t1, m2) : 0u);
+      const uint64_t inv0 = kIdxMask - q.key_off - (pb + 16u * (uint32_t)lane);
+      const uint32_t mh = m | sb.hi | (uint32_t)(inv0 >> 32);
+      const bool any = (m & 0x1fc00000u) && mh >= (uint32_t)(s.thr[sb.seg] >> 32) &&
+                       (sb.seg != wl.seg || mh > (uint32_t)(wl.thr >> 32));
+      if (__any_sync(0xffffffffu, any)) {
+        const uint32_t sa = sb.ts + 4u * s0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t vj = min((uint32_t)j < len1 ? t0 : t1, lds_u32(sa + 4u * j));
+          const uint64_t inv = inv0 - (uint64_t)j;
+          const uint64_t key = (vj & 0x1fc00000u)
+              ? (((uint64_t)(vj | sb.hi | (uint32_t)(inv >> 32)) << 32) | (uint32_t)inv) : 0ull;
+          wl_offer(key, key ? sb.seg : wl.seg, wl, lane, p.k, s.thr, s.list, s.lock, p.gthr);
+        }
+      }
+      return;
+    }
     uint32_t v[16];
     if (sb.ns >= 16) {
       const uint32_t r0 = fastdiv(o8, sb.ds), s0 = o8 - r0 * sb.ns;
