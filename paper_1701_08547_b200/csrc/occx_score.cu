@@ -659,6 +659,8 @@ struct SepBlock {            // warp-uniform description of the tabled block
   // what the tables were built for: (T, arch, REGS pool, SMEM pool, ok)
   uint32_t kt, ka, kr, ks;
   uint32_t rmq;              // bytes between the TS range-max levels (0: not built)
+  uint32_t rmq_k;            // top level: 4 (16-wide windows) or 5 (32-wide, TS padded by 31)
+  uint32_t rmq_ready;        // the levels for the current tables are built
 };
 
 __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
@@ -669,6 +671,21 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
 __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
+
+// Range-max levels over the padded TS (level k holds max(TS[i .. i + 2^k)),
+// k = 1 .. rmq_k, sb.rmq bytes apart; the padded length is the stride - 1).
+__device__ __forceinline__ void rmq_build(SepBlock& sb, int lane) {
+  const uint32_t len = sb.rmq / 4u - 1u;
+#pragma unroll 1
+  for (uint32_t k = 1; k <= sb.rmq_k; ++k) {
+    const uint32_t src = sb.ts + (k - 1) * sb.rmq, dst = sb.ts + k * sb.rmq, half = 1u << (k - 1);
+    for (uint32_t i = (uint32_t)lane; i + 2 * half <= len; i += 32)
+      sts_u32(dst + 4u * i, max(lds_u32(src + 4u * i), lds_u32(src + 4u * (i + half))));
+    __syncwarp();
+  }
+  sb.rmq_ready = 1;
+}
+
 
 // Fill TR[0, nR] and TS[0, nS + 7) (tr = the warp's table, shared address)
 // for the block ic points at; TR[nR] = 0 and TS[nS + t] = TS[t mod nS] pad
@@ -743,7 +760,10 @@ __device__ __forceinline__ bool sep_build(const SpaceParams& q, const K2Shared& 
       sts_u32(tr + 4u * i, ok ? (aw << 22) : 0u);
     }
     if (lane == 0) sts_u32(tr + 4u * nr, 0u);
-    for (uint32_t i = (uint32_t)lane; i < ns + 15; i += 32) {
+    // 32-candidate runs (levels up to 32-wide) when the padded tables fit
+    const bool wide = ns >= 32 && nr + 1 + 6 * (ns + 32) <= q.sep_words;
+    const uint32_t pad = wide ? 31u : 15u;
+    for (uint32_t i = (uint32_t)lane; i < ns + pad; i += 32) {
       const uint32_t S = pool[ic.s_off + i % ns];
       const uint32_t aw = min(sep_ls<MODE>(arch, S) * wpb, wmp);
       sts_u32(tr + 4u * (nr + 1 + i), ok ? (aw << 22) : 0u);
@@ -751,18 +771,14 @@ __device__ __forceinline__ bool sep_build(const SpaceParams& q, const K2Shared& 
     __syncwarp();
     // Range maxima over the padded TS for the quad filter: level k (k = 1..4)
     // holds max(TS[i .. i + 2^k)), levels ns + 16 words apart.
-    const uint32_t stride = 4u * (ns + 16);
+    const uint32_t stride = 4u * (ns + pad + 1);
+    const uint32_t top = wide ? 5u : 4u;
     sb.rmq = 0;
-    if (ns >= 16 && nr + 1 + 5 * (ns + 16) <= q.sep_words) {
-      const uint32_t ts = tr + 4u * (nr + 1);
-#pragma unroll 1
-      for (uint32_t k = 1; k <= 4; ++k) {
-        const uint32_t src = ts + (k - 1) * stride, dst = ts + k * stride, half = 1u << (k - 1);
-        for (uint32_t i = (uint32_t)lane; i + 2 * half <= ns + 15; i += 32)
-          sts_u32(dst + 4u * i, max(lds_u32(src + 4u * i), lds_u32(src + 4u * (i + half))));
-        __syncwarp();
-      }
+    sb.rmq_k = 0;
+    sb.rmq_ready = 0;              // levels are built on the first quad (rmq_build)
+    if (ns >= 16 && nr + 1 + (top + 1) * (ns + pad + 1) <= q.sep_words) {
       sb.rmq = stride;
+      sb.rmq_k = top;
     }
     sb.kt = kt;
     sb.ka = a;
@@ -813,6 +829,8 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
   sb.ns = 0;
   sb.kt = sb.ka = sb.kr = sb.ks = 0xffffffffu;          // no tables yet
   sb.rmq = 0;
+  sb.rmq_k = 0;
+  sb.rmq_ready = 0;
   BlockBound bbnd;
   bbnd.z = 0xffffffffu;
   bbnd.w = bbnd.r_off = bbnd.s_off = bbnd.aw = 0;
@@ -902,6 +920,29 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
         wl_offer(key, key ? sb.seg : wl.seg, wl, lane, p.k, s.thr, s.list, s.lock, p.gthr);
       }
     }
+  };
+  // Eight slices at `pb` as one filter: lane l's run is pb + 32l + j
+  // (j < 32), its bound from the 32-wide range maxima (|SMEM| >= 32: at most
+  // one REGS step in a run).  Only when some lane may offer are the eight
+  // slices scored as two quads (finer filters; the top-k does not depend on
+  // the order keys are offered in).
+  auto fast_oct = [&](uint64_t pb) {
+    const uint32_t o8 = (uint32_t)(pb - sb.lo) + 32u * (uint32_t)lane;
+    const uint32_t r0 = fastdiv(o8, sb.ds), s0 = o8 - r0 * sb.ns;
+    const uint32_t t0 = lds_u32(tr + 4u * r0), t1 = lds_u32(tr + 4u * r0 + 4u);
+    const uint32_t len1 = min(sb.ns - s0, 32u);          // >= 1
+    const uint32_t len2 = max(32u - len1, 1u);           // (1 when unused)
+    const uint32_t k1 = 31u - __clz(len1), k2 = 31u - __clz(len2);
+    const uint32_t l1 = sb.ts + k1 * sb.rmq, l2 = sb.ts + k2 * sb.rmq;
+    const uint32_t a2 = s0 + len1;
+    const uint32_t m1 = max(lds_u32(l1 + 4u * s0), lds_u32(l1 + 4u * (a2 - (1u << k1))));
+    const uint32_t m2 = max(lds_u32(l2 + 4u * a2), lds_u32(l2 + 4u * (a2 + len2 - (1u << k2))));
+    const uint32_t m = max(min(t0, m1), len1 < 32u ? min(t1, m2) : 0u);
+    const uint64_t inv0 = kIdxMask - q.key_off - (pb + 32u * (uint32_t)lane);
+    const uint32_t mh = m | sb.hi | (uint32_t)(inv0 >> 32);
+    const bool any = (m & 0x1fc00000u) && mh >= (uint32_t)(s.thr[sb.seg] >> 32) &&
+                     (sb.seg != wl.seg || mh > (uint32_t)(wl.thr >> 32));
+    return __any_sync(0xffffffffu, any);
   };
   auto fast_quad = [&](uint64_t pb) {
     const uint32_t o8 = (uint32_t)(pb - sb.lo) + 16u * (uint32_t)lane;
@@ -999,6 +1040,13 @@ __global__ void __launch_bounds__(kIgThreads, 1) score_space_kernel(const __grid
         const uint64_t lb = (sb.lo + sb.n - base) >> 7, lr = (we - base) >> 7;
         left = (uint32_t)(lb < lr ? lb : lr);
         // tight loop over the block's whole slices, two per trip
+        if (left >= 4 && sb.rmq && !sb.rmq_ready) rmq_build(sb, lane);
+        if (sb.rmq_k == 5)
+          for (; left >= 8; left -= 8, base += 1024)
+            if (fast_oct(base)) {
+              fast_quad(base);
+              fast_quad(base + 512);
+            }
         for (; left >= 4; left -= 4, base += 512) fast_quad(base);
         for (; left >= 2; left -= 2, base += 256) fast_pair(base);
         if (left) {                                        // an odd last slice
