@@ -684,8 +684,9 @@ def secondary_space_api(cfg, mode: str, steps: int = 10):
                                "instructions_per_launch": prof["warp_instructions"],
                                "peak_source": f"4 issue slots x {sms} SMs x {mhz} MHz (max SM clock)",
                                "alu_pipe_pct_ncu": prof.get("alu_pipe_pct"),
-                               "note": "the ALU pipe (ISETP/SEL/VIMNMX/LOP3) is the tighter "
-                                       "limit: alu_pipe_pct_ncu from the committed capture"}
+                               "note": "warp instructions per launch and the ALU-pipe share "
+                                       "from the committed ncu capture "
+                                       "(profiles/r02_k2i_ncu_full.json)"}
     except Exception as exc:
         out["roofline"] = {"error": repr(exc)[:160]}
     return out
